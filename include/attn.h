@@ -1,0 +1,195 @@
+/*
+ * attn.h -- C ABI of the B200 (sm_100a) fused-attention hot path of
+ * Neptune (arXiv 2510.08726): the reduction chain S = Q K^T -> score_mod/mask
+ * -> row max -> exp -> row sum -> O = P V computed in ONE naive-fusion pass
+ * over KV tiles with the algebraic repair term exp(m_old - m_new)
+ * ("Rolling Update", Alg. 1; tile form Fig. 19), and
+ * its loop-fission form for decoding with a repaired combine of partial
+ * (m, l, O) triples ("Split-K Update", Alg. 2; Fig. 5,
+ * P:706-722; Eq. 8).  P:n = line n of the paper's PAPER.md.
+ *
+ * The operation every entry point computes is Fig. 8's compute definition
+ * extended with the Table 1 variants:
+ *
+ *   x[i,j]   = scale * <q_i, k_j>                      (batch_matmul)
+ *   x[i,j]   = softcap * tanh(x / softcap)  if softcap > 0      (SoftCap)
+ *   x[i,j]  -= alibi_slopes[hq] * |qpos(i) - kpos(j)|  if slopes (ALiBi)
+ *   x[i,j]   = -inf  unless allowed(i,j)               (if_then_else)
+ *   O[i,:]   = sum_j exp(x[i,j] - m_i) v_j / sum_j exp(x[i,j] - m_i),
+ *              m_i = max_j x[i,j]
+ *   lse[i]   = m_i + ln(sum_j exp(x[i,j] - m_i))
+ *
+ *   qpos(i) = q_pos_offset + i,  kpos(j) = kv_pos_offset + j,
+ *   allowed = (!causal || kpos <= qpos)
+ *             && (window_left  < 0 || qpos - kpos <= window_left)
+ *             && (window_right < 0 || kpos - qpos <= window_right).
+ *   GQA: query head hq reads KV head hq / (heads_q / heads_kv).
+ *   A row with no allowed key has O = 0 and lse = -inf.
+ *
+ * Readings of points the paper leaves open are listed in DESIGN.md §2
+ * (R1..R12) and are binding for this ABI.
+ *
+ * Conventions for every call
+ * --------------------------
+ * - Tensors are caller-owned DEVICE memory, logical layout [B][H][S][D]
+ *   ("BHSD", Fig. 8's (B, N, S, H)) described by attn_tensor:
+ *   element strides for b, h, s; the D dimension must be contiguous.
+ *   bf16 tensors: base 16-byte aligned, strides multiples of 8 elements
+ *   (TMA requirement) -- else ATTN_ERR_ALIGNMENT.
+ * - Calls are asynchronous on `stream`; they never synchronise the host and
+ *   never allocate device memory, so they are CUDA-graph capturable.
+ * - Argument checks are synchronous and return a status; nothing is launched
+ *   when a check fails.  Launch failures map to ATTN_ERR_CUDA.  The detail
+ *   string of the last failure on the calling thread is attn_last_error().
+ * - There is no CPU fallback: unsupported combinations return
+ *   ATTN_ERR_UNSUPPORTED.
+ */
+#ifndef ATTN_H_
+#define ATTN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ATTN_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define ATTN_API __attribute__((visibility("default")))
+#else
+#define ATTN_API
+#endif
+
+typedef struct CUstream_st* attn_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+  ATTN_OK = 0,
+  ATTN_ERR_INVALID_ARGUMENT = 1,
+  ATTN_ERR_UNSUPPORTED = 2,
+  ATTN_ERR_ALIGNMENT = 3,
+  ATTN_ERR_WORKSPACE_TOO_SMALL = 4,
+  ATTN_ERR_CUDA = 5
+} attn_status;
+
+typedef enum {
+  ATTN_BF16 = 0, /* bf16 in/out, fp32 accumulation (tcgen05 / decode kernels) */
+  ATTN_FP32 = 1  /* fp32 in/out, fp32 SIMT path (head_dim <= 256) */
+} attn_dtype;
+
+/* A [B][H][S][D] view. Strides are in ELEMENTS of the tensor's dtype. */
+typedef struct {
+  void* ptr;
+  int64_t stride_b, stride_h, stride_s;
+} attn_tensor;
+
+/* Problem description shared by every call (Fig. 8 arguments + Table 1 variants). */
+typedef struct {
+  int32_t batch, heads_q, heads_kv;   /* heads_q % heads_kv == 0 (GQA group G) */
+  int32_t seqlen_q, seqlen_kv;        /* local extents of q and of k/v         */
+  int32_t head_dim;                   /* D: bf16 {64, 128}; fp32 1..256          */
+  attn_dtype dtype;
+  float scale;                        /* > 0, finite; configs use 1/sqrt(D)      */
+  float softcap;                      /* 0 = off; else > 0, finite               */
+  const float* alibi_slopes;          /* DEVICE fp32 [heads_q] or NULL           */
+  int32_t causal;                     /* 0/1                                     */
+  int32_t window_left, window_right;  /* -1 = unbounded, else >= 0               */
+  int64_t seqlen_kv_total;            /* 0 => seqlen_kv; else >= kv_pos_offset + seqlen_kv */
+  int64_t q_pos_offset;               /* INT64_MIN => seqlen_kv_total - seqlen_q (bottom-right) */
+  int64_t kv_pos_offset;              /* absolute position of local key 0 (KV shard start) */
+} attn_problem;
+
+#define ATTN_Q_POS_DEFAULT INT64_MIN
+
+/* Partial (m, l, O) triples of Split-K Update (Fig. 5 max_l / sum_l and the
+ * local PV).  fp32, DEVICE memory, caller-owned.  For part p, batch b,
+ * query head h:
+ *   m[p*m_stride_part + b*m_stride_b + h*m_stride_h]  = max_j x over the part (exact max;
+ *                                                        -inf if the part has no allowed key)
+ *   l[same index]                                     = sum_j exp(x - m)
+ *   o[p*o_stride_part + b*o_stride_b + h*o_stride_h + d] = sum_j exp(x - m) v_j[d]  (UN-normalised)
+ * m and l share strides.  Natural-log units (x as defined above). */
+typedef struct {
+  float* m;
+  float* l;
+  float* o;
+  int32_t num_parts;
+  int64_t m_stride_part, m_stride_b, m_stride_h;
+  int64_t o_stride_part, o_stride_b, o_stride_h;
+} attn_parts;
+
+/* ---------------------------------------------------------------------
+ * attn_fused_fwd -- Rolling Update forward / prefill (Alg. 1, Fig. 19).
+ *
+ * One pass over KV tiles per (b, hq, 128-row q tile): S_j = Q K_j^T on
+ * tcgen05 tensor cores into TMEM, score_mod/mask, running max, repair
+ * alpha = exp(m_old - m_new) applied to l and to the TMEM O accumulator
+ * (Eq. 7), O += P V_j, then O / l.
+ *   q [B][Hq][Sq][D], k/v [B][Hkv][Skv][D], o [B][Hq][Sq][D] (q's dtype).
+ *   lse: nullable DEVICE fp32 [B][Hq][Sq] contiguous.
+ * Errors: INVALID_ARGUMENT (extents < 1, heads_q % heads_kv, bad scale /
+ * softcap / window, offsets), ALIGNMENT, UNSUPPORTED (bf16 D not in {64,128};
+ * fp32 D > 256), CUDA.
+ * ------------------------------------------------------------------- */
+ATTN_API attn_status attn_fused_fwd(const attn_problem* prob, attn_tensor q, attn_tensor k, attn_tensor v,
+                           attn_tensor o, float* lse, attn_stream_t stream);
+
+/* ---------------------------------------------------------------------
+ * Split-K Update decode (Alg. 2, Fig. 5): seqlen_q must be 1, dtype bf16,
+ * D in {64, 128}.  The KV axis of every (b, hkv) is cut into num_splits
+ * contiguous parts (PrivatizeReduce); each CTA streams its part
+ * of K and V once from HBM for all G query heads of the group and emits one
+ * partial triple per (part, b, hq).  Then the global section (Eq. 8)
+ * combines them (attn_combine).
+ *
+ * attn_splitkv_default_splits: split count used when num_splits == 0
+ *   (enough (b, hkv, split) units to fill sm_count SMs).
+ * attn_splitkv_workspace_bytes: DEVICE workspace needed to hold the
+ *   partials when parts_out == NULL (pure host function).
+ * Part s covers local keys [s*L, min((s+1)*L, seqlen_kv)) with
+ *   L = 64 * ceil(ceil(seqlen_kv / num_splits) / 64)   (trailing parts may be
+ *   empty: m = -inf, l = 0, O = 0).
+ * attn_splitkv_decode: if parts_out != NULL the raw partials go there
+ *   (parts_out->num_parts must equal the split count) and no workspace is
+ *   needed; if o != NULL the normalised output (q's dtype) and lse (nullable)
+ *   are written after the combine.  At least one of parts_out / o must be set.
+ * ------------------------------------------------------------------- */
+ATTN_API int32_t attn_splitkv_default_splits(const attn_problem* prob, int32_t sm_count);
+ATTN_API size_t attn_splitkv_workspace_bytes(const attn_problem* prob, int32_t num_splits);
+ATTN_API attn_status attn_splitkv_decode(const attn_problem* prob, attn_tensor q, attn_tensor k, attn_tensor v,
+                                int32_t num_splits, void* workspace, size_t workspace_bytes,
+                                const attn_parts* parts_out, attn_tensor o, float* lse,
+                                attn_stream_t stream);
+
+/* ---------------------------------------------------------------------
+ * attn_combine -- the Split-K global section (Fig. 5 s_max_global /
+ * s_sum_global, Eq. 8) over in->num_parts partial triples per
+ * (b, h):  M = max_p m_p;  w_p = exp(m_p - M) (0 if m_p = -inf);
+ *          L = sum_p w_p l_p;  O = sum_p w_p O_p.
+ * Outputs (each nullable, at least one set):
+ *   o     : O / L in out_dtype ([B][H][1][D] view; 0 where L = 0)
+ *   lse   : M + ln L, fp32 [B][H] contiguous (-inf where L = 0)
+ *   acc_out: the UN-normalised merged triple (num_parts must be 1), used to
+ *            merge hierarchically (splits within a GPU, then GPUs).
+ * Valid because h commutes with the reducer (Eq. 4).
+ * ------------------------------------------------------------------- */
+ATTN_API attn_status attn_combine(int32_t batch, int32_t heads, int32_t head_dim, const attn_parts* in,
+                         attn_dtype out_dtype, attn_tensor o, float* lse, const attn_parts* acc_out,
+                         attn_stream_t stream);
+
+/* ---------------------------------------------------------------------
+ * Seeded synthetic inputs are produced by a separate library (datagen/);
+ * nothing here generates data.  Introspection:
+ * ------------------------------------------------------------------- */
+ATTN_API const char* attn_status_string(attn_status s);
+ATTN_API const char* attn_last_error(void);   /* thread-local detail of the last non-OK status */
+ATTN_API int attn_abi_version(void);
+/* Number of kernels the last successful call on this thread enqueued (for
+ * launch accounting in bench.py). */
+ATTN_API int attn_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ATTN_H_ */

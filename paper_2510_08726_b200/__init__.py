@@ -1,0 +1,214 @@
+"""B200-native (sm_100a) hot path of Neptune (arXiv 2510.08726): fused
+attention by Rolling Update (prefill) and Split-K Update (decode).
+
+This module is argument marshalling only: every arithmetic step runs in the
+CUDA kernels of ``libattn.so`` behind the C ABI in ``include/attn.h``.
+PyTorch supplies device memory and streams.  There is no CPU fallback: if the
+library is missing or a configuration is unsupported, the call raises.
+
+Tensors use the BHSD layout of the paper's Fig. 8:
+q [B, Hq, Sq, D], k/v [B, Hkv, Skv, D], D contiguous.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from typing import Optional, Tuple
+
+import torch
+
+from . import _ffi
+from ._ffi import AttnParts, AttnProblem, AttnTensor, check, load
+
+__all__ = ["fused_fwd", "splitkv_decode", "combine", "default_splits", "workspace_bytes",
+           "last_launch_count", "Parts", "load"]
+
+_DT = {torch.bfloat16: _ffi.ATTN_BF16, torch.float32: _ffi.ATTN_FP32}
+
+
+def _as_tensor(t: Optional[torch.Tensor]) -> AttnTensor:
+    if t is None:
+        return AttnTensor(None, 0, 0, 0)
+    if t.dim() != 4 or t.stride(3) != 1:
+        raise ValueError("expected a [B, H, S, D] tensor with a contiguous last dimension")
+    return AttnTensor(t.data_ptr(), t.stride(0), t.stride(1), t.stride(2))
+
+
+def _stream(stream) -> ctypes.c_void_p:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _problem(q, k, *, scale, causal, window, alibi_slopes, softcap, q_pos_offset, kv_pos_offset,
+             seqlen_kv_total) -> AttnProblem:
+    B, Hq, Sq, D = q.shape
+    Bk, Hkv, Skv, Dk = k.shape
+    if Bk != B or Dk != D:
+        raise ValueError("q and k disagree on batch or head_dim")
+    if q.dtype not in _DT:
+        raise ValueError(f"unsupported dtype {q.dtype}")
+    if alibi_slopes is not None:
+        if alibi_slopes.dtype != torch.float32 or alibi_slopes.device != q.device or alibi_slopes.numel() != Hq:
+            raise ValueError("alibi_slopes must be a float32 tensor [Hq] on q's device")
+    return AttnProblem(
+        batch=B, heads_q=Hq, heads_kv=Hkv, seqlen_q=Sq, seqlen_kv=Skv, head_dim=D, dtype=_DT[q.dtype],
+        scale=float(1.0 / math.sqrt(D) if scale is None else scale), softcap=float(softcap),
+        alibi_slopes=None if alibi_slopes is None else alibi_slopes.data_ptr(), causal=int(bool(causal)),
+        window_left=int(window[0]), window_right=int(window[1]),
+        seqlen_kv_total=int(seqlen_kv_total or 0),
+        q_pos_offset=_ffi.ATTN_Q_POS_DEFAULT if q_pos_offset is None else int(q_pos_offset),
+        kv_pos_offset=int(kv_pos_offset))
+
+
+def last_launch_count() -> int:
+    """Kernels enqueued by the last successful call on this thread."""
+    return load().attn_last_launch_count()
+
+
+def fused_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: Optional[float] = None,
+              causal: bool = False, window: Tuple[int, int] = (-1, -1),
+              alibi_slopes: Optional[torch.Tensor] = None, softcap: float = 0.0,
+              q_pos_offset: Optional[int] = None, kv_pos_offset: int = 0,
+              seqlen_kv_total: Optional[int] = None, out: Optional[torch.Tensor] = None,
+              lse: Optional[torch.Tensor] = None, return_lse: bool = False, stream=None):
+    """Rolling Update forward (``attn_fused_fwd``).
+
+    Device tensors run in place on ``stream``.  Host (CPU) tensors take the
+    end-to-end path: copied to the current device, computed, copied back
+    (pinned host memory makes the copies asynchronous)."""
+    lib = load()
+    if q.device.type == "cpu":
+        dev = torch.device("cuda", torch.cuda.current_device())
+        qd, kd, vd = (t.to(dev, non_blocking=True) for t in (q, k, v))
+        sl = None if alibi_slopes is None else alibi_slopes.to(dev, non_blocking=True)
+        res = fused_fwd(qd, kd, vd, scale=scale, causal=causal, window=window, alibi_slopes=sl, softcap=softcap,
+                        q_pos_offset=q_pos_offset, kv_pos_offset=kv_pos_offset, seqlen_kv_total=seqlen_kv_total,
+                        return_lse=return_lse, stream=stream)
+        if return_lse:
+            o_d, l_d = res
+            return (o_d.to("cpu", non_blocking=False) if out is None else out.copy_(o_d)), l_d.cpu()
+        return res.to("cpu") if out is None else out.copy_(res)
+    prob = _problem(q, k, scale=scale, causal=causal, window=window, alibi_slopes=alibi_slopes, softcap=softcap,
+                    q_pos_offset=q_pos_offset, kv_pos_offset=kv_pos_offset, seqlen_kv_total=seqlen_kv_total)
+    if out is None:
+        out = torch.empty_like(q, memory_format=torch.contiguous_format)
+    if return_lse and lse is None:
+        lse = torch.empty(q.shape[:3], device=q.device, dtype=torch.float32)
+    if lse is not None and (not lse.is_contiguous() or lse.dtype != torch.float32):
+        raise ValueError("lse must be a contiguous float32 [B, Hq, Sq] tensor")
+    check(lib.attn_fused_fwd(ctypes.byref(prob), _as_tensor(q), _as_tensor(k), _as_tensor(v), _as_tensor(out),
+                             None if lse is None else lse.data_ptr(), _stream(stream)), "attn_fused_fwd")
+    return (out, lse) if return_lse else out
+
+
+class Parts:
+    """Partial (m, l, O) triples of Split-K Update (Fig. 5): m, l [P, B, H]
+    and o [P, B, H, D] fp32 views (any strides with a contiguous D)."""
+
+    def __init__(self, m: torch.Tensor, l: torch.Tensor, o: torch.Tensor):
+        if m.stride() != l.stride():
+            raise ValueError("m and l must share strides")
+        if o.stride(3) != 1:
+            raise ValueError("o must be contiguous over D")
+        self.m, self.l, self.o = m, l, o
+
+    @staticmethod
+    def empty(P: int, B: int, H: int, D: int, device) -> "Parts":
+        return Parts(torch.empty(P, B, H, device=device), torch.empty(P, B, H, device=device),
+                     torch.empty(P, B, H, D, device=device))
+
+    @staticmethod
+    def packed(buf: torch.Tensor) -> "Parts":
+        """Views over one [P, B, H, D + 2] fp32 buffer: O at [..., :D], m at D, l at D + 1
+        (the all-gather layout of the KV-sharded decode)."""
+        D = buf.shape[-1] - 2
+        return Parts(buf[..., D], buf[..., D + 1], buf[..., :D])
+
+    def c(self) -> AttnParts:
+        m, o = self.m, self.o
+        return AttnParts(m.data_ptr(), self.l.data_ptr(), o.data_ptr(), m.shape[0], m.stride(0), m.stride(1),
+                         m.stride(2), o.stride(0), o.stride(1), o.stride(2))
+
+
+def default_splits(q: torch.Tensor, k: torch.Tensor, sm_count: int = 0) -> int:
+    prob = _problem(q, k, scale=None, causal=False, window=(-1, -1), alibi_slopes=None, softcap=0.0,
+                    q_pos_offset=None, kv_pos_offset=0, seqlen_kv_total=None)
+    return load().attn_splitkv_default_splits(ctypes.byref(prob), sm_count)
+
+
+def workspace_bytes(q: torch.Tensor, k: torch.Tensor, num_splits: int = 0) -> int:
+    prob = _problem(q, k, scale=None, causal=False, window=(-1, -1), alibi_slopes=None, softcap=0.0,
+                    q_pos_offset=None, kv_pos_offset=0, seqlen_kv_total=None)
+    return load().attn_splitkv_workspace_bytes(ctypes.byref(prob), num_splits)
+
+
+def splitkv_decode(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, num_splits: int = 0,
+                   scale: Optional[float] = None, causal: bool = False, window: Tuple[int, int] = (-1, -1),
+                   alibi_slopes: Optional[torch.Tensor] = None, softcap: float = 0.0,
+                   q_pos_offset: Optional[int] = None, kv_pos_offset: int = 0,
+                   seqlen_kv_total: Optional[int] = None, out: Optional[torch.Tensor] = None,
+                   lse: Optional[torch.Tensor] = None, return_lse: bool = False, parts: Optional[Parts] = None,
+                   workspace: Optional[torch.Tensor] = None, want_out: bool = True, stream=None):
+    """Split-K Update decode (``attn_splitkv_decode``): q [B, Hq, 1, D] bf16.
+
+    ``parts`` receives the raw local-section triples; with ``want_out`` the
+    Eq. 8 combine also produces O (and lse)."""
+    lib = load()
+    if q.device.type == "cpu":
+        dev = torch.device("cuda", torch.cuda.current_device())
+        qd, kd, vd = (t.to(dev, non_blocking=True) for t in (q, k, v))
+        sl = None if alibi_slopes is None else alibi_slopes.to(dev, non_blocking=True)
+        res = splitkv_decode(qd, kd, vd, num_splits=num_splits, scale=scale, causal=causal, window=window,
+                             alibi_slopes=sl, softcap=softcap, q_pos_offset=q_pos_offset,
+                             kv_pos_offset=kv_pos_offset, seqlen_kv_total=seqlen_kv_total, return_lse=return_lse,
+                             stream=stream)
+        if return_lse:
+            return res[0].cpu(), res[1].cpu()
+        return res.cpu()
+    prob = _problem(q, k, scale=scale, causal=causal, window=window, alibi_slopes=alibi_slopes, softcap=softcap,
+                    q_pos_offset=q_pos_offset, kv_pos_offset=kv_pos_offset, seqlen_kv_total=seqlen_kv_total)
+    if num_splits == 0:
+        num_splits = lib.attn_splitkv_default_splits(ctypes.byref(prob), 0)
+    if want_out and out is None:
+        out = torch.empty_like(q, memory_format=torch.contiguous_format)
+    if not want_out:
+        out = None
+    if return_lse and lse is None and want_out:
+        lse = torch.empty(q.shape[:2], device=q.device, dtype=torch.float32)
+    ws_ptr, ws_bytes = None, 0
+    if parts is None:
+        need = lib.attn_splitkv_workspace_bytes(ctypes.byref(prob), num_splits)
+        if workspace is None or workspace.numel() * workspace.element_size() < need:
+            workspace = torch.empty(need, dtype=torch.uint8, device=q.device)
+        ws_ptr, ws_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
+    cparts = None if parts is None else ctypes.byref(parts.c())
+    check(lib.attn_splitkv_decode(ctypes.byref(prob), _as_tensor(q), _as_tensor(k), _as_tensor(v), num_splits,
+                                  ws_ptr, ws_bytes, cparts, _as_tensor(out), None if lse is None else lse.data_ptr(),
+                                  _stream(stream)), "attn_splitkv_decode")
+    if not want_out:
+        return parts
+    return (out, lse) if return_lse else out
+
+
+def combine(parts: Parts, *, out: Optional[torch.Tensor] = None, out_dtype=torch.bfloat16,
+            lse: Optional[torch.Tensor] = None, return_lse: bool = False, acc: Optional[Parts] = None,
+            want_out: bool = True, stream=None):
+    """Split-K global section (``attn_combine``, Eq. 8) over parts [P, B, H(, D)].
+
+    ``out`` gets O / L as [B, H, 1, D]; ``acc`` (num_parts = 1) gets the
+    un-normalised merged triple for a further hierarchical merge."""
+    lib = load()
+    P, B, H, D = parts.o.shape
+    if want_out and out is None:
+        out = torch.empty(B, H, 1, D, device=parts.o.device, dtype=out_dtype)
+    if not want_out:
+        out = None
+    if return_lse and lse is None:
+        lse = torch.empty(B, H, device=parts.o.device, dtype=torch.float32)
+    dt = _DT[out.dtype] if out is not None else _ffi.ATTN_FP32
+    cacc = None if acc is None else ctypes.byref(acc.c())
+    check(lib.attn_combine(B, H, D, ctypes.byref(parts.c()), dt, _as_tensor(out),
+                           None if lse is None else lse.data_ptr(), cacc, _stream(stream)), "attn_combine")
+    if return_lse:
+        return out, lse
+    return out

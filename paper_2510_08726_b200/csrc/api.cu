@@ -1,0 +1,336 @@
+// api.cu -- host side of the C ABI declared in include/attn.h: argument
+// validation (synchronous status codes, no exceptions), TMA descriptor
+// construction (cuTensorMapEncodeTiled through the runtime's driver entry
+// point, so the library links no libcuda), and kernel dispatch.  No device
+// memory is allocated here and the host never synchronises.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/attn.h"
+#include "kernels.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+thread_local int g_launches = 0;
+
+attn_status fail(attn_status s, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+#define CHECK_ARG(cond, ...) \
+  do {                       \
+    if (!(cond)) return fail(ATTN_ERR_INVALID_ARGUMENT, __VA_ARGS__); \
+  } while (0)
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// 4-D bf16 map over [B][H][S][D] (dims listed innermost first), box (box_d, box_s, 1, 1).
+attn_status make_map(CUtensorMap* m, const attn_tensor& t, int B, int H, int S, int D, int box_d, int box_s,
+                     bool swizzle128) {
+  EncodeFn enc = get_encode();
+  if (!enc) return fail(ATTN_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)S, (cuuint64_t)H, (cuuint64_t)B};
+  cuuint64_t strides[3] = {(cuuint64_t)t.stride_s * 2, (cuuint64_t)t.stride_h * 2, (cuuint64_t)t.stride_b * 2};
+  cuuint32_t box[4] = {(cuuint32_t)box_d, (cuuint32_t)box_s, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, t.ptr, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ATTN_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return ATTN_OK;
+}
+
+attn_status check_tensor(const attn_tensor& t, const char* name, int elem_bytes, int B, int H, int S) {
+  if (t.ptr == nullptr) return fail(ATTN_ERR_INVALID_ARGUMENT, "%s: null pointer", name);
+  if (t.stride_b < 0 || t.stride_h < 0 || t.stride_s < 0)
+    return fail(ATTN_ERR_INVALID_ARGUMENT, "%s: negative stride", name);
+  if (elem_bytes == 2) {
+    if ((reinterpret_cast<uintptr_t>(t.ptr) & 15) != 0)
+      return fail(ATTN_ERR_ALIGNMENT, "%s: base pointer must be 16-byte aligned", name);
+    if ((B > 1 && t.stride_b % 8) || (H > 1 && t.stride_h % 8) || (S > 1 && t.stride_s % 8))
+      return fail(ATTN_ERR_ALIGNMENT, "%s: strides must be multiples of 8 elements (16 bytes)", name);
+  } else if ((reinterpret_cast<uintptr_t>(t.ptr) & 3) != 0) {
+    return fail(ATTN_ERR_ALIGNMENT, "%s: base pointer must be 4-byte aligned", name);
+  }
+  return ATTN_OK;
+}
+
+attn_status check_problem(const attn_problem* p, attn::VariantParams* vp) {
+  CHECK_ARG(p != nullptr, "problem is NULL");
+  CHECK_ARG(p->batch >= 1 && p->heads_q >= 1 && p->heads_kv >= 1 && p->seqlen_q >= 1 && p->seqlen_kv >= 1 &&
+                p->head_dim >= 1,
+            "all extents must be >= 1");
+  CHECK_ARG(p->heads_q % p->heads_kv == 0, "heads_q (%d) must be a multiple of heads_kv (%d)", p->heads_q,
+            p->heads_kv);
+  CHECK_ARG(isfinite(p->scale) && p->scale > 0.f, "scale must be finite and > 0");
+  CHECK_ARG(isfinite(p->softcap) && p->softcap >= 0.f, "softcap must be finite and >= 0");
+  CHECK_ARG(p->window_left >= -1 && p->window_right >= -1, "window bounds must be >= -1");
+  CHECK_ARG(p->causal == 0 || p->causal == 1, "causal must be 0 or 1");
+  CHECK_ARG(p->dtype == ATTN_BF16 || p->dtype == ATTN_FP32, "unknown dtype");
+  const int64_t total = p->seqlen_kv_total == 0 ? p->seqlen_kv : p->seqlen_kv_total;
+  CHECK_ARG(p->kv_pos_offset >= 0 && p->kv_pos_offset + p->seqlen_kv <= total,
+            "need 0 <= kv_pos_offset and kv_pos_offset + seqlen_kv <= seqlen_kv_total");
+  CHECK_ARG(total < (1LL << 30) && p->seqlen_q < (1 << 30), "sequence too long");
+  const int64_t qoff = p->q_pos_offset == ATTN_Q_POS_DEFAULT ? total - p->seqlen_q : p->q_pos_offset;
+  CHECK_ARG(qoff > -(1LL << 30) && qoff < (1LL << 30), "q_pos_offset out of range");
+  const float log2e = 1.4426950408889634f;
+  vp->scale = p->scale;
+  vp->scale_log2 = p->scale * log2e;
+  vp->softcap = p->softcap;
+  vp->softcap_log2 = p->softcap * log2e;
+  vp->scale_over_cap = p->softcap > 0.f ? p->scale / p->softcap : 0.f;
+  vp->alibi = p->alibi_slopes;
+  vp->causal = p->causal;
+  vp->window_left = p->window_left;
+  vp->window_right = p->window_right;
+  vp->q_off = qoff;
+  vp->kv_off = p->kv_pos_offset;
+  return ATTN_OK;
+}
+
+attn_status cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return ATTN_OK;
+  return fail(ATTN_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+int sm_count_cached() {
+  static int n = 0;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) n = 148;
+  });
+  return n;
+}
+
+attn::Shape shape_of(const attn_problem* p) {
+  return attn::Shape{p->batch, p->heads_q, p->heads_kv, p->seqlen_q, p->seqlen_kv, p->head_dim};
+}
+
+}  // namespace
+
+extern "C" {
+
+int attn_abi_version(void) { return ATTN_ABI_VERSION; }
+const char* attn_last_error(void) { return g_err; }
+int attn_last_launch_count(void) { return g_launches; }
+
+const char* attn_status_string(attn_status s) {
+  switch (s) {
+    case ATTN_OK: return "ok";
+    case ATTN_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case ATTN_ERR_UNSUPPORTED: return "unsupported";
+    case ATTN_ERR_ALIGNMENT: return "alignment";
+    case ATTN_ERR_WORKSPACE_TOO_SMALL: return "workspace too small";
+    case ATTN_ERR_CUDA: return "cuda error";
+  }
+  return "unknown status";
+}
+
+attn_status attn_fused_fwd(const attn_problem* prob, attn_tensor q, attn_tensor k, attn_tensor v, attn_tensor o,
+                           float* lse, attn_stream_t stream) {
+  g_err[0] = 0;
+  attn::VariantParams vp;
+  attn_status st = check_problem(prob, &vp);
+  if (st != ATTN_OK) return st;
+  const attn_problem& p = *prob;
+  const int eb = p.dtype == ATTN_BF16 ? 2 : 4;
+  if ((st = check_tensor(q, "q", eb, p.batch, p.heads_q, p.seqlen_q)) != ATTN_OK) return st;
+  if ((st = check_tensor(k, "k", eb, p.batch, p.heads_kv, p.seqlen_kv)) != ATTN_OK) return st;
+  if ((st = check_tensor(v, "v", eb, p.batch, p.heads_kv, p.seqlen_kv)) != ATTN_OK) return st;
+  if ((st = check_tensor(o, "o", eb, p.batch, p.heads_q, p.seqlen_q)) != ATTN_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int launches = 0;
+  if (p.dtype == ATTN_BF16) {
+    if (p.head_dim != 64 && p.head_dim != 128)
+      return fail(ATTN_ERR_UNSUPPORTED, "bf16 head_dim must be 64 or 128 (got %d)", p.head_dim);
+    attn::FwdTcArgs a;
+    a.s = shape_of(prob);
+    a.v = vp;
+    a.lse = lse;
+    if ((st = make_map(&a.tm_q, q, p.batch, p.heads_q, p.seqlen_q, p.head_dim, 64, 128, true)) != ATTN_OK) return st;
+    if ((st = make_map(&a.tm_k, k, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, 128, true)) != ATTN_OK) return st;
+    if ((st = make_map(&a.tm_v, v, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, 128, true)) != ATTN_OK) return st;
+    if ((st = make_map(&a.tm_o, o, p.batch, p.heads_q, p.seqlen_q, p.head_dim, 64, 128, true)) != ATTN_OK) return st;
+    st = cuda_status(attn::launch_fwd_tc(a, s, &launches), "fwd_tc launch");
+  } else {
+    if (p.head_dim > 256) return fail(ATTN_ERR_UNSUPPORTED, "fp32 head_dim must be <= 256");
+    attn::FwdSimtArgs a;
+    a.s = shape_of(prob);
+    a.v = vp;
+    a.q = static_cast<const float*>(q.ptr);
+    a.k = static_cast<const float*>(k.ptr);
+    a.v_ = static_cast<const float*>(v.ptr);
+    a.o = static_cast<float*>(o.ptr);
+    a.q_sb = q.stride_b; a.q_sh = q.stride_h; a.q_ss = q.stride_s;
+    a.k_sb = k.stride_b; a.k_sh = k.stride_h; a.k_ss = k.stride_s;
+    a.v_sb = v.stride_b; a.v_sh = v.stride_h; a.v_ss = v.stride_s;
+    a.o_sb = o.stride_b; a.o_sh = o.stride_h; a.o_ss = o.stride_s;
+    a.lse = lse;
+    st = cuda_status(attn::launch_fwd_simt(a, s, &launches), "fwd_simt launch");
+  }
+  if (st == ATTN_OK) g_launches = launches;
+  return st;
+}
+
+int32_t attn_splitkv_default_splits(const attn_problem* p, int32_t sm_count) {
+  if (p == nullptr || p->batch < 1 || p->heads_kv < 1 || p->seqlen_kv < 1) return 1;
+  if (sm_count <= 0) sm_count = sm_count_cached();
+  const int nk = attn::decode_stage_keys(p->heads_q / p->heads_kv, p->head_dim);
+  const int64_t units = (int64_t)p->batch * p->heads_kv;
+  const int64_t target = 2LL * sm_count;   // two resident CTAs per SM
+  int64_t splits = (target + units - 1) / units;
+  const int64_t max_splits = (p->seqlen_kv + nk - 1) / nk;
+  if (splits > max_splits) splits = max_splits;
+  if (splits < 1) splits = 1;
+  return (int32_t)splits;
+}
+
+size_t attn_splitkv_workspace_bytes(const attn_problem* p, int32_t num_splits) {
+  if (p == nullptr) return 0;
+  if (num_splits <= 0) num_splits = attn_splitkv_default_splits(p, 0);
+  const size_t rows = (size_t)num_splits * p->batch * p->heads_q;
+  auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
+  return up(rows * 4) * 2 + up(rows * p->head_dim * 4);
+}
+
+attn_status attn_splitkv_decode(const attn_problem* prob, attn_tensor q, attn_tensor k, attn_tensor v,
+                                int32_t num_splits, void* workspace, size_t workspace_bytes,
+                                const attn_parts* parts_out, attn_tensor o, float* lse, attn_stream_t stream) {
+  g_err[0] = 0;
+  attn::VariantParams vp;
+  attn_status st = check_problem(prob, &vp);
+  if (st != ATTN_OK) return st;
+  const attn_problem& p = *prob;
+  if (p.seqlen_q != 1) return fail(ATTN_ERR_UNSUPPORTED, "decode requires seqlen_q == 1 (got %d)", p.seqlen_q);
+  if (p.dtype != ATTN_BF16) return fail(ATTN_ERR_UNSUPPORTED, "decode supports bf16 only");
+  if (p.head_dim != 64 && p.head_dim != 128)
+    return fail(ATTN_ERR_UNSUPPORTED, "decode head_dim must be 64 or 128 (got %d)", p.head_dim);
+  const int G = p.heads_q / p.heads_kv;
+  if (G > 8) return fail(ATTN_ERR_UNSUPPORTED, "decode supports GQA groups up to 8 (got %d)", G);
+  CHECK_ARG(parts_out != nullptr || o.ptr != nullptr, "decode needs parts_out or o");
+  if (num_splits < 0) return fail(ATTN_ERR_INVALID_ARGUMENT, "num_splits must be >= 0");
+  if (num_splits == 0) num_splits = attn_splitkv_default_splits(prob, 0);
+  if ((st = check_tensor(q, "q", 2, p.batch, p.heads_q, 1)) != ATTN_OK) return st;
+  if ((st = check_tensor(k, "k", 2, p.batch, p.heads_kv, p.seqlen_kv)) != ATTN_OK) return st;
+  if ((st = check_tensor(v, "v", 2, p.batch, p.heads_kv, p.seqlen_kv)) != ATTN_OK) return st;
+  if (o.ptr != nullptr && (st = check_tensor(o, "o", 2, p.batch, p.heads_q, 1)) != ATTN_OK) return st;
+
+  attn::DecodeArgs a;
+  a.s = shape_of(prob);
+  a.v = vp;
+  a.q = static_cast<const uint16_t*>(q.ptr);
+  a.q_sb = q.stride_b;
+  a.q_sh = q.stride_h;
+  const int nk = attn::decode_stage_keys(G, p.head_dim);
+  a.num_splits = num_splits;
+  const int64_t per = (p.seqlen_kv + num_splits - 1) / num_splits;
+  a.split_len = (int)(((per + nk - 1) / nk) * nk);
+  if (parts_out != nullptr) {
+    CHECK_ARG(parts_out->m && parts_out->l && parts_out->o, "parts_out has a null array");
+    CHECK_ARG(parts_out->num_parts == num_splits, "parts_out->num_parts (%d) must equal the split count (%d)",
+              parts_out->num_parts, num_splits);
+    a.parts = attn::PartsView{parts_out->m, parts_out->l, parts_out->o, num_splits,
+                              parts_out->m_stride_part, parts_out->m_stride_b, parts_out->m_stride_h,
+                              parts_out->o_stride_part, parts_out->o_stride_b, parts_out->o_stride_h};
+  } else {
+    const size_t need = attn_splitkv_workspace_bytes(prob, num_splits);
+    if (workspace == nullptr || workspace_bytes < need)
+      return fail(ATTN_ERR_WORKSPACE_TOO_SMALL, "workspace needs %zu bytes", need);
+    const size_t rows = (size_t)num_splits * p.batch * p.heads_q;
+    auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
+    char* w = static_cast<char*>(workspace);
+    float* m = reinterpret_cast<float*>(w);
+    float* l = reinterpret_cast<float*>(w + up(rows * 4));
+    float* ob = reinterpret_cast<float*>(w + 2 * up(rows * 4));
+    const long long bh = (long long)p.batch * p.heads_q;
+    a.parts = attn::PartsView{m, l, ob, num_splits, bh, p.heads_q, 1, bh * p.head_dim,
+                              (long long)p.heads_q * p.head_dim, p.head_dim};
+  }
+  if ((st = make_map(&a.tm_k, k, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, nk, true)) != ATTN_OK) return st;
+  if ((st = make_map(&a.tm_v, v, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, nk, true)) != ATTN_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int launches = 0;
+  st = cuda_status(attn::launch_decode(a, s, &launches), "decode launch");
+  if (st != ATTN_OK) return st;
+  if (o.ptr != nullptr) {
+    attn::CombineArgs c{};
+    c.B = p.batch;
+    c.H = p.heads_q;
+    c.D = p.head_dim;
+    c.in = a.parts;
+    c.out_bf16 = 1;
+    c.o = o.ptr;
+    c.o_sb = o.stride_b;
+    c.o_sh = o.stride_h;
+    c.lse = lse;
+    c.acc.m = nullptr;
+    st = cuda_status(attn::launch_combine(c, s, &launches), "combine launch");
+  }
+  if (st == ATTN_OK) g_launches = launches;
+  return st;
+}
+
+attn_status attn_combine(int32_t batch, int32_t heads, int32_t head_dim, const attn_parts* in,
+                         attn_dtype out_dtype, attn_tensor o, float* lse, const attn_parts* acc_out,
+                         attn_stream_t stream) {
+  g_err[0] = 0;
+  CHECK_ARG(batch >= 1 && heads >= 1 && head_dim >= 1, "extents must be >= 1");
+  if (head_dim > 256) return fail(ATTN_ERR_UNSUPPORTED, "combine head_dim must be <= 256");
+  CHECK_ARG(in != nullptr && in->m && in->l && in->o && in->num_parts >= 1, "bad input parts");
+  CHECK_ARG(o.ptr != nullptr || lse != nullptr || acc_out != nullptr, "no output requested");
+  CHECK_ARG(out_dtype == ATTN_BF16 || out_dtype == ATTN_FP32, "unknown out dtype");
+  if (acc_out) CHECK_ARG(acc_out->m && acc_out->l && acc_out->o && acc_out->num_parts == 1, "bad acc_out");
+  attn::CombineArgs c{};
+  c.B = batch;
+  c.H = heads;
+  c.D = head_dim;
+  c.in = attn::PartsView{in->m, in->l, in->o, in->num_parts, in->m_stride_part, in->m_stride_b, in->m_stride_h,
+                         in->o_stride_part, in->o_stride_b, in->o_stride_h};
+  c.out_bf16 = out_dtype == ATTN_BF16;
+  c.o = o.ptr;
+  c.o_sb = o.stride_b;
+  c.o_sh = o.stride_h;
+  c.lse = lse;
+  if (acc_out)
+    c.acc = attn::PartsView{acc_out->m, acc_out->l, acc_out->o, 1, 0, acc_out->m_stride_b, acc_out->m_stride_h,
+                            0, acc_out->o_stride_b, acc_out->o_stride_h};
+  else
+    c.acc.m = nullptr;
+  int launches = 0;
+  attn_status st = cuda_status(attn::launch_combine(c, reinterpret_cast<cudaStream_t>(stream), &launches),
+                               "combine launch");
+  if (st == ATTN_OK) g_launches = launches;
+  return st;
+}
+
+}  // extern "C"

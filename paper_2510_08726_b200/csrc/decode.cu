@@ -1,0 +1,369 @@
+// decode.cu -- Split-K Update for decoding (Alg. 2; Fig. 5,
+// P:706-722) and its global repair-combine (Eq. 8).
+//
+// Local section (decode_split_kernel): one CTA per (split, hkv, b).  The KV
+// axis of (b, hkv) is privatised into contiguous splits (FuseAndPrivatize,
+// P:673-677); the CTA streams its split of K and V from HBM exactly once
+// through a TMA ring (128-byte swizzled [keys x 64] boxes) and computes, for
+// all G = Hq / Hkv query heads of the group at once, the local max m_s, the
+// local sum l_s = sum exp(x - m_s) and the un-normalised PV_s.  Inside a split
+// each warp runs a rolling update over 16-key sub-tiles (Fig. 19), and the
+// four warps' states are merged with the Eq. 8 algebra at the end.
+//
+// Decode is HBM-bound (4 flop per K/V byte at G = 4).  The G query heads are
+// packed as rows of a 16-row mma.sync tile with the unused rows zero ("uses
+// masks to apply TensorCore ... too few input matrix rows"), so
+// the CUDA cores only do the softmax and the instruction budget per streamed
+// byte stays far below the issue rate.
+//
+// Global section (combine_kernel): per (b, h): M = max_s m_s, w_s =
+// exp(m_s - M), L = sum w_s l_s, O = sum w_s O_s; output O / L and
+// lse = M + ln L, or the un-normalised merged triple for hierarchical merges.
+#include <cuda_bf16.h>
+#include <math.h>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace attn {
+namespace {
+
+constexpr int kConsumerWarps = 4;
+constexpr int kKeysPerWarp = 16;
+constexpr int NK = kConsumerWarps * kKeysPerWarp;  // keys per stage
+constexpr int kStages = 3;
+constexpr int kThreads = (kConsumerWarps + 1) * 32;
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr float kLog2e = 1.4426950408889634f;
+
+template <int D>
+struct DCfg {
+  static constexpr int kBoxes = D / 64;
+  static constexpr int kTileBytes = NK * D * 2;               // one K (or V) stage tile
+  static constexpr int kStageBytes = 2 * kTileBytes;
+  static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + 2 * kStages * 8 + 64;
+};
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// Byte offset of 16-byte chunk `ch` (0 .. D/8-1) of row `key` in a stage tile
+// made of D/64 TMA boxes of [NK rows x 128 B] with the 128-byte swizzle.
+__device__ __forceinline__ uint32_t tile_off(int key, int ch) {
+  return (ch >> 3) * (NK * 128) + key * 128 + (((ch & 7) ^ (key & 7)) << 4);
+}
+
+template <int D, bool kAlibi, bool kSoftcap>
+__global__ void __launch_bounds__(kThreads) decode_split_kernel(const __grid_constant__ CUtensorMap tm_k,
+                                                                const __grid_constant__ CUtensorMap tm_v,
+                                                                const DecodeArgs a) {
+  using C = DCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * C::kStageBytes);
+  uint64_t* empty = full + kStages;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int split = blockIdx.x, hkv = blockIdx.y, b = blockIdx.z;
+  const int G = a.s.Hq / a.s.Hkv;
+  const int ks = split * a.split_len;
+  const int ke = min(ks + a.split_len, a.s.Skv);
+  const int nstage = ke > ks ? (ke - ks + NK - 1) / NK : 0;
+
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&tm_k);
+    prefetch_tmap(&tm_v);
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kConsumerWarps);
+    }
+    fence_mbarrier_init();
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();   // K/V are streamed exactly once
+      for (int st = 0; st < nstage; ++st) {
+        const int slot = st % kStages;
+        mbar_wait(&empty[slot], ((st / kStages) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[slot], C::kStageBytes);
+        uint8_t* dst = smem + slot * C::kStageBytes;
+        for (int bx = 0; bx < C::kBoxes; ++bx) {
+          tma_load_4d(&tm_k, &full[slot], dst + bx * NK * 128, bx * 64, ks + st * NK, hkv, b, pol);
+          tma_load_4d(&tm_v, &full[slot], dst + C::kTileBytes + bx * NK * 128, bx * 64, ks + st * NK, hkv, b, pol);
+        }
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------ consumers
+  const VariantParams& v = a.v;
+  const int row = lane >> 2;          // mma row = query head within the group (rows >= G are padding)
+  const int quad = lane & 3;
+  const bool row_ok = row < G;
+  const int hq = hkv * G + (row_ok ? row : 0);
+  const long long qpos = v.q_off;     // Sq = 1
+  // Q as the A operand: rows = heads (zero beyond G); loaded once.
+  uint32_t qa[D / 16][4];
+  {
+    const uint16_t* qrow = a.q + (long long)b * a.q_sb + (long long)hq * a.q_sh;
+#pragma unroll
+    for (int kk = 0; kk < D / 16; ++kk) {
+      const int d0 = kk * 16 + quad * 2;
+      qa[kk][0] = row_ok ? *reinterpret_cast<const uint32_t*>(qrow + d0) : 0u;
+      qa[kk][1] = 0u;  // rows 8..15
+      qa[kk][2] = row_ok ? *reinterpret_cast<const uint32_t*>(qrow + d0 + 8) : 0u;
+      qa[kk][3] = 0u;
+    }
+  }
+  // allowed key interval of this query (local indices), intersected with the split
+  long long jlo = ks, jhi = ke - 1;
+  if (v.window_left >= 0) jlo = max(jlo, qpos - v.window_left - v.kv_off);
+  if (v.causal) jhi = min(jhi, qpos - v.kv_off);
+  if (v.window_right >= 0) jhi = min(jhi, qpos + v.window_right - v.kv_off);
+  const float nslope2 = (kAlibi && row_ok) ? -v.alibi[hq] * kLog2e : 0.f;
+
+  float m = -INFINITY;   // running max of this warp's keys for row `row` (log2 units)
+  float l = 0.f;         // per-thread partial of the running denominator
+  float o[D / 8][4];
+#pragma unroll
+  for (int n = 0; n < D / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+
+  for (int st = 0; st < nstage; ++st) {
+    const int slot = st % kStages;
+    mbar_wait(&full[slot], (st / kStages) & 1);
+    const uint32_t sk = smem_u32(smem + slot * C::kStageBytes);
+    const uint32_t sv = sk + C::kTileBytes;
+    const int kb = warp * kKeysPerWarp;   // this warp's 16 keys of the stage
+
+    // S (16 rows x 16 keys) = Q K^T
+    float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    {
+      const int key = kb + (lane & 7) + ((lane >> 4) << 3);
+      const int sub = (lane >> 3) & 1;
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(sk + tile_off(key, kk * 2 + sub), b0, b1, b2, b3);
+        mma16816(s[0], qa[kk], b0, b1);
+        mma16816(s[1], qa[kk], b2, b3);
+      }
+    }
+    // score_mod + mask (log2 units); this thread holds keys kb + n*8 + quad*2 + e of row `row`
+    const int key0 = ks + st * NK + kb;
+    float x[4];
+#pragma unroll
+    for (int n = 0; n < 2; ++n)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = key0 + n * 8 + quad * 2 + e;
+        float xv = s[n][e];
+        if constexpr (kSoftcap) {
+          xv = v.softcap_log2 * tanh_approx(xv * v.scale_over_cap);
+        } else {
+          xv *= v.scale_log2;
+        }
+        if constexpr (kAlibi) xv = fmaf(nslope2, fabsf((float)(qpos - v.kv_off - j)), xv);
+        x[n * 2 + e] = (j >= jlo && j <= jhi && row_ok) ? xv : -INFINITY;
+      }
+    float mt = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
+    mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 1));
+    mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 2));
+    const float m_new = fmaxf(m, mt);
+    // repair term exp(m_old - m_new) (Fig. 18d); guards for rows still empty
+    const float alpha = (m == -INFINITY) ? 0.f : ex2_approx(m - m_new);
+    const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
+    float p[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) p[e] = ex2_approx(x[e] - m_use);
+    l = l * alpha + (p[0] + p[1] + p[2] + p[3]);
+    m = m_new;
+#pragma unroll
+    for (int n = 0; n < D / 8; ++n) {
+      o[n][0] *= alpha;
+      o[n][1] *= alpha;
+    }
+    // P as the A operand (rows 8..15 zero)
+    uint32_t pa[4];
+    pa[0] = pack_bf16x2(p[0], p[1]);
+    pa[1] = 0u;
+    pa[2] = pack_bf16x2(p[2], p[3]);
+    pa[3] = 0u;
+    // O (16 x D) += P V
+    {
+      const int key = kb + (lane & 7) + (((lane >> 3) & 1) << 3);
+      const int sub = lane >> 4;
+#pragma unroll
+      for (int nd = 0; nd < D / 8; nd += 2) {
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(sv + tile_off(key, nd + sub), b0, b1, b2, b3);
+        mma16816(o[nd], pa, b0, b1);
+        mma16816(o[nd + 1], pa, b2, b3);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+  }
+
+  // ------------------------------------------------------------ merge the 4 warps (Eq. 8) and emit
+  l += __shfl_xor_sync(0xffffffffu, l, 1);
+  l += __shfl_xor_sync(0xffffffffu, l, 2);
+  // every stage's smem is free now: reuse it for the reduction
+  named_bar_sync(1, kConsumerWarps * 32);
+  float* red = reinterpret_cast<float*>(smem);   // [warp][16 rows][D + 2]
+  float* rw = red + (warp * 16 + row) * (D + 2);
+#pragma unroll
+  for (int n = 0; n < D / 8; ++n) {
+    rw[n * 8 + quad * 2] = o[n][0];
+    rw[n * 8 + quad * 2 + 1] = o[n][1];
+  }
+  if (quad == 0) {
+    rw[D] = m;
+    rw[D + 1] = l;
+  }
+  named_bar_sync(1, kConsumerWarps * 32);
+  for (int e = threadIdx.x; e < G * D; e += kConsumerWarps * 32) {
+    const int h = e / D, d = e % D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, red[(w * 16 + h) * (D + 2) + D]);
+    float L = 0.f, O = 0.f;
+    if (M != -INFINITY) {
+#pragma unroll
+      for (int w = 0; w < kConsumerWarps; ++w) {
+        const float* r = red + (w * 16 + h) * (D + 2);
+        const float mw = r[D];
+        const float wgt = (mw == -INFINITY) ? 0.f : ex2_approx(mw - M);
+        L = fmaf(wgt, r[D + 1], L);
+        O = fmaf(wgt, r[d], O);
+      }
+    }
+    const int hh = hkv * G + h;
+    float* po = a.parts.o + split * a.parts.o_sp + (long long)b * a.parts.o_sb + (long long)hh * a.parts.o_sh;
+    po[d] = O;
+    if (d == 0) {
+      const long long mi = split * a.parts.m_sp + (long long)b * a.parts.m_sb + (long long)hh * a.parts.m_sh;
+      a.parts.m[mi] = M * kLn2;   // natural-log units (ABI)
+      a.parts.l[mi] = L;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- Eq. 8 combine
+__global__ void __launch_bounds__(128) combine_kernel(const CombineArgs a) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int idx = blockIdx.x * 4 + warp;   // (b, h)
+  if (idx >= a.B * a.H) return;
+  const int b = idx / a.H, h = idx % a.H;
+  const PartsView& in = a.in;
+  const long long mb = (long long)b * in.m_sb + (long long)h * in.m_sh;
+  const long long ob = (long long)b * in.o_sb + (long long)h * in.o_sh;
+  float M = -INFINITY;
+  for (int p = lane; p < in.num_parts; p += 32) M = fmaxf(M, in.m[p * in.m_sp + mb]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  float L = 0.f;
+  constexpr int kMaxDL = 8;   // D <= 256
+  float acc[kMaxDL];
+#pragma unroll
+  for (int r = 0; r < kMaxDL; ++r) acc[r] = 0.f;
+  if (M != -INFINITY) {
+    for (int p = 0; p < in.num_parts; ++p) {
+      const float mp = in.m[p * in.m_sp + mb];
+      if (mp == -INFINITY) continue;            // w_p = 0 for empty parts
+      const float w = expf(mp - M);              // repair term exp(max_l - max_g)
+      L = fmaf(w, in.l[p * in.m_sp + mb], L);
+      const float* op = in.o + p * in.o_sp + ob;
+#pragma unroll
+      for (int r = 0; r < kMaxDL; ++r) {
+        const int d = lane + 32 * r;
+        if (d < a.D) acc[r] = fmaf(w, op[d], acc[r]);
+      }
+    }
+  }
+  if (a.o) {
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+#pragma unroll
+    for (int r = 0; r < kMaxDL; ++r) {
+      const int d = lane + 32 * r;
+      if (d >= a.D) continue;
+      const long long oi = (long long)b * a.o_sb + (long long)h * a.o_sh + d;
+      if (a.out_bf16)
+        reinterpret_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(acc[r] * inv);
+      else
+        reinterpret_cast<float*>(a.o)[oi] = acc[r] * inv;
+    }
+  }
+  if (a.lse && lane == 0) a.lse[(long long)b * a.H + h] = L > 0.f ? M + logf(L) : -INFINITY;
+  if (a.acc.m) {
+    const long long mi = (long long)b * a.acc.m_sb + (long long)h * a.acc.m_sh;
+    if (lane == 0) {
+      a.acc.m[mi] = L > 0.f ? M : -INFINITY;
+      a.acc.l[mi] = L;
+    }
+    float* po = a.acc.o + (long long)b * a.acc.o_sb + (long long)h * a.acc.o_sh;
+#pragma unroll
+    for (int r = 0; r < kMaxDL; ++r) {
+      const int d = lane + 32 * r;
+      if (d < a.D) po[d] = acc[r];
+    }
+  }
+}
+
+template <int D, bool kAlibi, bool kSoftcap>
+cudaError_t launch_dec_t(const DecodeArgs& a, cudaStream_t stream) {
+  using C = DCfg<D>;
+  auto kern = decode_split_kernel<D, kAlibi, kSoftcap>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+  if (e != cudaSuccess) return e;
+  dim3 grid(a.num_splits, a.s.Hkv, a.s.B);
+  kern<<<grid, kThreads, C::kSmemBytes, stream>>>(a.tm_k, a.tm_v, a);
+  return cudaGetLastError();
+}
+
+template <int D>
+cudaError_t launch_dec_d(const DecodeArgs& a, cudaStream_t stream) {
+  const bool alibi = a.v.alibi != nullptr, cap = a.v.softcap > 0.f;
+  if (alibi && cap) return launch_dec_t<D, true, true>(a, stream);
+  if (alibi) return launch_dec_t<D, true, false>(a, stream);
+  if (cap) return launch_dec_t<D, false, true>(a, stream);
+  return launch_dec_t<D, false, false>(a, stream);
+}
+
+}  // namespace
+
+int decode_stage_keys(int, int) { return NK; }
+
+cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t stream, int* launches) {
+  cudaError_t e = a.s.D == 128 ? launch_dec_d<128>(a, stream) : launch_dec_d<64>(a, stream);
+  if (e == cudaSuccess && launches) ++*launches;
+  return e;
+}
+
+cudaError_t launch_combine(const CombineArgs& a, cudaStream_t stream, int* launches) {
+  const int n = a.B * a.H;
+  combine_kernel<<<(n + 3) / 4, 128, 0, stream>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && launches) ++*launches;
+  return e;
+}
+
+}  // namespace attn

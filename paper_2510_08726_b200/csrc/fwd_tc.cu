@@ -1,0 +1,443 @@
+// fwd_tc.cu -- Rolling Update forward (prefill) on sm_100a tensor cores.
+//
+// The paper's Rolling Update (Alg. 1) fuses the attention
+// reduction chain of Fig. 8 into ONE loop over KV tiles; the
+// tile-level loop body is Fig. 19: local max, global max,
+// repair term h(t, r, r') = exp(r - r') t (Fig. 18d) applied to
+// the running sum and to the PV accumulator (Eq. 7), local exp
+// sum, PV, then m_old <- m_new (Alg. 1 CacheReducePrevResult);
+// O / l after the loop (Fig. 9 reverse_compute_at(norm)).
+//
+// B200 mapping:
+//   CTA = 2 query tiles of BM = 128 rows of one (b, hq) -> 256 rows; 384 threads.
+//   warp 0      : TMA producer (Q once; K_j / V_j through a ring of kStages slots)
+//   warp 1      : tcgen05.mma issuer (one thread)
+//   warp 2      : TMEM allocator (512 columns)
+//   warps 4-7   : softmax/correction/epilogue for query tile 0 (thread = row)
+//   warps 8-11  : same for query tile 1
+//   TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512) (fp32 columns);
+//         P_t (bf16) overwrites the first 64 columns of S_t and feeds the
+//         PV MMA straight from TMEM (A operand in TMEM).
+//   MMA issue order per KV step j: PV0(j), QK0(j+1), PV1(j), QK1(j+1), so the
+//   tensor core runs one tile's MMAs while the other tile's softmax runs.
+//   Repair is lazy (reading R9): the reference max r' only moves when the
+//   running max exceeds it by more than kTau (log2 units); exact because h
+//   tag-updates to any reference (Eq. 6).
+#include <math.h>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace attn {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BN = 128;
+constexpr int kThreads = 384;
+constexpr float kTau = 8.0f;
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr float kLog2e = 1.4426950408889634f;
+
+template <int D>
+struct Cfg {
+  static constexpr int kBoxes = D / 64;           // 64-column (128 B) swizzle atoms per row
+  static constexpr int kQTileBytes = BM * D * 2;
+  static constexpr int kKVTileBytes = BN * D * 2;
+  static constexpr int kStages = (D == 128) ? 4 : 8;
+  static constexpr int kSmemQ = 2 * kQTileBytes;
+  static constexpr int kSmemKV = kStages * kKVTileBytes;
+  static constexpr int kNumBars = 1 + 2 * kStages + 6;
+  static constexpr int kSmemBytes = 1024 + kSmemQ + kSmemKV + kNumBars * 8 + 16;
+};
+
+struct Range {
+  int lo, hi;                      // active KV tiles [lo, hi)
+  int jlo_first, jhi_first;        // allowed key interval of the first row
+  int jlo_last, jhi_last;          // ... and of the last valid row
+};
+
+// Allowed local key interval [jlo, jhi] of a query at absolute position qp
+// (mask definition in include/attn.h), clamped to [0, Skv - 1].
+__device__ __forceinline__ void row_bounds(const Shape& s, const VariantParams& v, long long qp, int& jlo,
+                                           int& jhi) {
+  long long lo = 0, hi = s.Skv - 1;
+  if (v.window_left >= 0) lo = max(lo, qp - v.window_left - v.kv_off);
+  const long long kInf = 0x3fffffffffffffffLL;
+  long long h = kInf;
+  if (v.causal) h = qp;
+  if (v.window_right >= 0) h = min(h, qp + (long long)v.window_right);
+  if (h != kInf) hi = min(hi, h - v.kv_off);
+  jlo = (int)min(lo, (long long)s.Skv);
+  jhi = (int)max(hi, -1LL);
+}
+
+__device__ __forceinline__ Range tile_range(const Shape& s, const VariantParams& v, int i0) {
+  Range r{0, 0, 0, -1, 0, -1};
+  if (i0 >= s.Sq) return r;
+  const int il = min(i0 + BM, s.Sq) - 1;
+  row_bounds(s, v, v.q_off + i0, r.jlo_first, r.jhi_first);
+  row_bounds(s, v, v.q_off + il, r.jlo_last, r.jhi_last);
+  if (r.jlo_first <= r.jhi_last) {
+    r.lo = r.jlo_first / BN;
+    r.hi = r.jhi_last / BN + 1;
+  }
+  return r;
+}
+
+__device__ __forceinline__ bool active(const Range& r, int j) { return j >= r.lo && j < r.hi; }
+
+__device__ __forceinline__ float u2f(uint32_t u) { return __uint_as_float(u); }
+__device__ __forceinline__ uint32_t f2u(float f) { return __float_as_uint(f); }
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15, %16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+
+// score_mod + mask of one S row (BN raw fp32 dots in `x`), in place, into the
+// log2 domain used by the exponentials; returns the row max of the tile.
+// Plain variant: x stays raw (scale folded into the exp FFMA) and the max is
+// rescaled afterwards (scale > 0 so max commutes with it).
+template <bool kAlibi, bool kSoftcap, bool kMask>
+__device__ __forceinline__ float score_tile(float (&x)[BN], const VariantParams& v, float nslope2, float dq0,
+                                            int rel_lo, int rel_hi) {
+  float mt = -INFINITY;
+#pragma unroll
+  for (int c = 0; c < BN; ++c) {
+    float xv = x[c];
+    if constexpr (kSoftcap) {
+      xv = v.softcap_log2 * tanh_approx(xv * v.scale_over_cap);   // R3: cap * tanh(x / cap)
+    } else if constexpr (kAlibi) {
+      xv = xv * v.scale_log2;
+    }
+    if constexpr (kAlibi) xv = fmaf(nslope2, fabsf(dq0 - (float)c), xv);  // R4: -slope |qpos - kpos|
+    if constexpr (kMask) xv = (c >= rel_lo && c <= rel_hi) ? xv : -INFINITY;
+    x[c] = xv;
+    mt = fmaxf(mt, xv);
+  }
+  if constexpr (!kAlibi && !kSoftcap) mt *= v.scale_log2;
+  return mt;
+}
+
+template <int D, bool kAlibi, bool kSoftcap>
+__global__ void __launch_bounds__(kThreads, 1)
+    fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                  const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o, const Shape s,
+                  const VariantParams v, float* __restrict__ lse) {
+  using C = Cfg<D>;
+  constexpr bool kPlain = !kAlibi && !kSoftcap;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sKV = smem + C::kSmemQ;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::kSmemKV);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = kv_full + C::kStages;
+  uint64_t* s_full = kv_empty + C::kStages;
+  uint64_t* p_ready = s_full + 2;
+  uint64_t* o_done = p_ready + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int qblk = v.causal ? (int)(gridDim.x - 1 - blockIdx.x) : (int)blockIdx.x;  // heavy causal tiles first
+  const int hq = blockIdx.y, b = blockIdx.z;
+  const int hkv = hq / (s.Hq / s.Hkv);                       // R6: contiguous GQA groups
+  const int row0 = qblk * 2 * BM;
+  const Range rng0 = tile_range(s, v, row0), rng1 = tile_range(s, v, row0 + BM);
+  const bool has_rows1 = row0 + BM < s.Sq;
+  int ulo = 0, uhi = 0;
+  if (rng0.hi > rng0.lo && rng1.hi > rng1.lo) {
+    ulo = min(rng0.lo, rng1.lo);
+    uhi = max(rng0.hi, rng1.hi);
+  } else if (rng0.hi > rng0.lo) {
+    ulo = rng0.lo; uhi = rng0.hi;
+  } else if (rng1.hi > rng1.lo) {
+    ulo = rng1.lo; uhi = rng1.hi;
+  }
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tm_q);
+    prefetch_tmap(&tm_k);
+    prefetch_tmap(&tm_v);
+    prefetch_tmap(&tm_o);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < C::kStages; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_ready[t], 4);
+      mbar_init(&o_done[t], 1);
+    }
+    fence_mbarrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint64_t pol_q = policy_evict_first();
+      const uint64_t pol_kv = policy_evict_last();   // K/V are re-read by the other q-blocks of this head
+      const int nq = has_rows1 ? 2 : 1;
+      mbar_arrive_expect_tx(q_full, nq * C::kQTileBytes);
+      for (int t = 0; t < nq; ++t)
+        for (int bx = 0; bx < C::kBoxes; ++bx)
+          tma_load_4d(&tm_q, q_full, sQ + t * C::kQTileBytes + bx * BM * 128, bx * 64, row0 + t * BM, hq, b, pol_q);
+      int it = 0;
+      for (int j = ulo; j < uhi; ++j) {
+        for (int kind = 0; kind < 2; ++kind, ++it) {
+          const int slot = it % C::kStages;
+          mbar_wait(&kv_empty[slot], ((it / C::kStages) & 1) ^ 1);
+          mbar_arrive_expect_tx(&kv_full[slot], C::kKVTileBytes);
+          uint8_t* dst = sKV + slot * C::kKVTileBytes;
+          const CUtensorMap* tm = kind == 0 ? &tm_k : &tm_v;
+          for (int bx = 0; bx < C::kBoxes; ++bx)
+            tma_load_4d(tm, &kv_full[slot], dst + bx * BN * 128, bx * 64, j * BN, hkv, b, pol_kv);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0 && uhi > ulo) {
+      constexpr uint32_t idesc_qk = idesc_bf16_f32(BM, BN, 0, 0);  // Q K-major, K K-major
+      constexpr uint32_t idesc_pv = idesc_bf16_f32(BM, D, 0, 1);   // P (TMEM), V MN-major
+      const uint32_t tS[2] = {tmem, tmem + 128};
+      const uint32_t tO[2] = {tmem + 256, tmem + 384};
+      const Range rg[2] = {rng0, rng1};
+      uint32_t p_phase[2] = {0, 0};
+      mbar_wait(q_full, 0);
+
+      auto wait_slot = [&](int it) {
+        mbar_wait(&kv_full[it % C::kStages], (it / C::kStages) & 1);
+        tc_fence_after();
+      };
+      auto qk = [&](int t, int it) {
+        const uint32_t sq = smem_u32(sQ + t * C::kQTileBytes);
+        const uint32_t sk = smem_u32(sKV + (it % C::kStages) * C::kKVTileBytes);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t ka = (kk >> 2) * (BM * 128) + (kk & 3) * 32;
+          const uint32_t kb = (kk >> 2) * (BN * 128) + (kk & 3) * 32;
+          mma_ss(tS[t], smem_desc_sw128(sq + ka, 16, 1024), smem_desc_sw128(sk + kb, 16, 1024), idesc_qk,
+                 kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&s_full[t]);
+      };
+      auto pv = [&](int t, int it, bool acc) {
+        mbar_wait(&p_ready[t], p_phase[t]);
+        p_phase[t] ^= 1;
+        tc_fence_after();
+        const uint32_t sv = smem_u32(sKV + (it % C::kStages) * C::kKVTileBytes);
+#pragma unroll
+        for (int kk = 0; kk < BN / 16; ++kk)
+          mma_ts(tO[t], tS[t] + kk * 8, smem_desc_sw128(sv + kk * 2048, BN * 128, 1024), idesc_pv,
+                 (acc || kk > 0) ? 1u : 0u);
+        mma_commit(&o_done[t]);
+      };
+
+      wait_slot(0);
+      if (active(rg[0], ulo)) qk(0, 0);
+      if (active(rg[1], ulo)) qk(1, 0);
+      mma_commit(&kv_empty[0]);
+      for (int j = ulo; j < uhi; ++j) {
+        const int itV = 2 * (j - ulo) + 1, itK1 = itV + 1;
+        const bool more = j + 1 < uhi;
+        wait_slot(itV);
+        if (active(rg[0], j)) pv(0, itV, j > rg[0].lo);
+        if (more) {
+          wait_slot(itK1);
+          if (active(rg[0], j + 1)) qk(0, itK1);
+        }
+        if (active(rg[1], j)) pv(1, itV, j > rg[1].lo);
+        mma_commit(&kv_empty[itV % C::kStages]);
+        if (more) {
+          if (active(rg[1], j + 1)) qk(1, itK1);
+          mma_commit(&kv_empty[itK1 % C::kStages]);
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax / correction / epilogue
+    const int t = (int)(warp - 4) >> 2;
+    const int wq = warp & 3;
+    const int r = wq * 32 + lane;
+    const Range R = t == 0 ? rng0 : rng1;
+    const int i = row0 + t * BM + r;
+    const long long qpos = v.q_off + i;
+    int jlo_row, jhi_row;
+    row_bounds(s, v, qpos, jlo_row, jhi_row);
+    const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
+    const uint32_t tS = tmem + t * 128 + lane_off;
+    const uint32_t tO = tmem + 256 + t * 128 + lane_off;
+    const float nslope2 = kAlibi ? -v.alibi[hq] * kLog2e : 0.f;
+    float m_ref = -INFINITY;  // stale reference max (log2 units), R9
+    float l = 0.f;            // running denominator (sum of un-rounded fp32 p, R10)
+
+    for (int j = R.lo; j < R.hi; ++j) {
+      const int it = j - R.lo;
+      mbar_wait(&s_full[t], it & 1);
+      tc_fence_after();
+      float x[BN];
+      {
+        uint32_t u[BN];
+#pragma unroll
+        for (int c = 0; c < BN / 32; ++c) tmem_ld32(tS + c * 32, reinterpret_cast<uint32_t(&)[32]>(u[c * 32]));
+        tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < BN; ++c) x[c] = u2f(u[c]);
+      }
+      // Fig. 19 max_local (+ score_mod, mask) -> max_global
+      const bool need_mask = !(j * BN >= R.jlo_last && (j + 1) * BN - 1 <= R.jhi_first);
+      const int rel_lo = jlo_row - j * BN, rel_hi = jhi_row - j * BN;
+      const float dq0 = (float)(qpos - v.kv_off - (long long)j * BN);
+      const float mt = need_mask ? score_tile<kAlibi, kSoftcap, true>(x, v, nslope2, dq0, rel_lo, rel_hi)
+                                 : score_tile<kAlibi, kSoftcap, false>(x, v, nslope2, dq0, rel_lo, rel_hi);
+      const float m_run = fmaxf(m_ref, mt);
+      bool move, need_o;
+      if (m_ref == -INFINITY) {
+        move = m_run != -INFINITY;
+        need_o = false;          // nothing accumulated yet for this row
+      } else {
+        move = m_run - m_ref > kTau;
+        need_o = move;
+      }
+      float alpha = 1.f;
+      if (need_o) alpha = ex2_approx(m_ref - m_run);   // repair term h = exp(r - r') (Fig. 18d)
+      if (move) m_ref = m_run;
+      l *= alpha;                                       // xsum = h(xsum) + ...
+      // exp(x - m), local sum, P -> bf16 into TMEM (aliasing S)
+      const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
+      float sum = 0.f;
+#pragma unroll
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          float p0, p1;
+          if constexpr (kPlain) {
+            p0 = ex2_approx(fmaf(x[c0 + 2 * e], v.scale_log2, -m_use));
+            p1 = ex2_approx(fmaf(x[c0 + 2 * e + 1], v.scale_log2, -m_use));
+          } else {
+            p0 = ex2_approx(x[c0 + 2 * e] - m_use);
+            p1 = ex2_approx(x[c0 + 2 * e + 1] - m_use);
+          }
+          sum += p0 + p1;
+          pk[e] = pack_bf16x2(p0, p1);
+        }
+        tmem_st16(tS + c0 / 2, pk);
+      }
+      // (done after P so the S registers are dead; PV(j) cannot start before p_ready)
+      if (__any_sync(0xffffffffu, need_o)) {
+        // O = h(O): wait for PV of the previous tile, then rescale the TMEM accumulator.
+        mbar_wait(&o_done[t], (it - 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t o[32];
+          tmem_ld32(tO + c * 32, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] = f2u(u2f(o[e]) * alpha);
+          tmem_st32(tO + c * 32, o);
+        }
+        tmem_st_wait();
+      }
+      tmem_st_wait();
+      l += sum;
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_ready[t]);
+    }
+
+    // ------------------------------------------------------------ epilogue: O / l -> bf16 -> TMA store
+    const int n_it = R.hi - R.lo;
+    const bool tile_rows = (row0 + t * BM) < s.Sq;
+    if (tile_rows) {
+      if (n_it > 0) {
+        mbar_wait(&o_done[t], (n_it - 1) & 1);
+        tc_fence_after();
+      } else {
+        mbar_wait(q_full, 0);   // the Q tile we overwrite must have landed
+      }
+      const float inv_l = l > 0.f ? 1.f / l : 0.f;
+      uint8_t* sOut = sQ + t * C::kQTileBytes;
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t o[32];
+        if (n_it > 0) {
+          tmem_ld32(tO + c * 32, o);
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] = 0u;
+        }
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) pk[e] = pack_bf16x2(u2f(o[2 * e]) * inv_l, u2f(o[2 * e + 1]) * inv_l);
+        uint8_t* rowp = sOut + (c >> 1) * (BM * 128) + r * 128;
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const int ch = (c & 1) * 4 + q4;
+          *reinterpret_cast<uint4*>(rowp + ((ch ^ (r & 7)) << 4)) =
+              make_uint4(pk[4 * q4], pk[4 * q4 + 1], pk[4 * q4 + 2], pk[4 * q4 + 3]);
+        }
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(1 + t, 128);
+      if (wq == 0 && lane == 0) {
+        for (int bx = 0; bx < C::kBoxes; ++bx) tma_store_4d(&tm_o, sOut + bx * BM * 128, bx * 64, row0 + t * BM, hq, b);
+        bulk_commit();
+        bulk_wait_read0();
+      }
+      if (lse != nullptr && i < s.Sq)
+        lse[((size_t)b * s.Hq + hq) * s.Sq + i] = l > 0.f ? m_ref * kLn2 + logf(l) : -INFINITY;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+template <int D, bool kAlibi, bool kSoftcap>
+cudaError_t launch_t(const FwdTcArgs& a, cudaStream_t stream) {
+  using C = Cfg<D>;
+  auto kern = fwd_tc_kernel<D, kAlibi, kSoftcap>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+  if (e != cudaSuccess) return e;
+  dim3 grid((a.s.Sq + 2 * BM - 1) / (2 * BM), a.s.Hq, a.s.B);
+  kern<<<grid, kThreads, C::kSmemBytes, stream>>>(a.tm_q, a.tm_k, a.tm_v, a.tm_o, a.s, a.v, a.lse);
+  return cudaGetLastError();
+}
+
+template <int D>
+cudaError_t launch_d(const FwdTcArgs& a, cudaStream_t stream) {
+  const bool alibi = a.v.alibi != nullptr, cap = a.v.softcap > 0.f;
+  if (alibi && cap) return launch_t<D, true, true>(a, stream);
+  if (alibi) return launch_t<D, true, false>(a, stream);
+  if (cap) return launch_t<D, false, true>(a, stream);
+  return launch_t<D, false, false>(a, stream);
+}
+
+}  // namespace
+
+cudaError_t launch_fwd_tc(const FwdTcArgs& a, cudaStream_t stream, int* launches) {
+  cudaError_t e = a.s.D == 128 ? launch_d<128>(a, stream) : launch_d<64>(a, stream);
+  if (e == cudaSuccess && launches) ++*launches;
+  return e;
+}
+
+}  // namespace attn

@@ -1,0 +1,77 @@
+// kernels.h -- internal (non-ABI) launch interface between the host layer
+// (api.cu) and the kernels.  Not installed; no torch types anywhere.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace attn {
+
+// Variant parameters shared by all kernels, pre-converted on the host to the
+// log2 domain the kernels compute in (exp(x) = exp2(x * log2 e)).
+struct VariantParams {
+  float scale;          // softmax scale on q.k
+  float scale_log2;     // scale * log2(e)
+  float softcap;        // 0 = off
+  float softcap_log2;   // softcap * log2(e)
+  float scale_over_cap; // scale / softcap
+  const float* alibi;   // natural-units slopes [Hq] or nullptr
+  int causal;
+  int window_left, window_right;
+  long long q_off;      // absolute position of query row 0
+  long long kv_off;     // absolute position of local key 0
+};
+
+struct Shape {
+  int B, Hq, Hkv, Sq, Skv, D;
+};
+
+// ------------------------------------------------------------ tcgen05 prefill
+struct FwdTcArgs {
+  Shape s;
+  VariantParams v;
+  float* lse;  // nullable, [B][Hq][Sq]
+  CUtensorMap tm_q, tm_k, tm_v, tm_o;
+};
+cudaError_t launch_fwd_tc(const FwdTcArgs& a, cudaStream_t stream, int* launches);
+
+// ------------------------------------------------------------ fp32 SIMT forward
+struct FwdSimtArgs {
+  Shape s;
+  VariantParams v;
+  const float* q; const float* k; const float* v_; float* o;
+  long long q_sb, q_sh, q_ss, k_sb, k_sh, k_ss, v_sb, v_sh, v_ss, o_sb, o_sh, o_ss;
+  float* lse;
+};
+cudaError_t launch_fwd_simt(const FwdSimtArgs& a, cudaStream_t stream, int* launches);
+
+// ------------------------------------------------------------ split-KV decode
+struct PartsView {
+  float* m; float* l; float* o;
+  int num_parts;
+  long long m_sp, m_sb, m_sh, o_sp, o_sb, o_sh;
+};
+struct DecodeArgs {
+  Shape s;
+  VariantParams v;
+  const uint16_t* q;            // bf16 bits
+  long long q_sb, q_sh;
+  int num_splits, split_len;    // keys per split (multiple of the stage size)
+  PartsView parts;              // destination of the local-section triples
+  CUtensorMap tm_k, tm_v;       // [D x Skv x Hkv x B], box (D, NK)
+};
+cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t stream, int* launches);
+int decode_stage_keys(int G, int D);
+
+// ------------------------------------------------------------ combine (Eq. 8)
+struct CombineArgs {
+  int B, H, D;
+  PartsView in;
+  int out_bf16;                 // 1: bf16 out, 0: fp32 out
+  void* o; long long o_sb, o_sh;  // nullable
+  float* lse;                   // nullable [B][H]
+  PartsView acc;                // acc.m == nullptr => not written
+};
+cudaError_t launch_combine(const CombineArgs& a, cudaStream_t stream, int* launches);
+
+}  // namespace attn
