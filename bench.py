@@ -1,0 +1,398 @@
+#!/usr/bin/env python
+"""Benchmark of the Neptune attention hot path on B200 (driver contract).
+
+Headline (BASELINE.json metric): attention forward TFLOP/s and % of BF16
+peak on the MHA prefill config (B=8, H=16, S=4096, D=128, non-causal, bf16)
+through the tcgen05 Rolling Update kernel; a secondary ``decode`` object
+reports split-KV decode HBM GB/s on config 5 (Hq=32, Hkv=8, KV 128K, D=128).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...    (one process per GPU)
+
+Multi-GPU: prefill shards independent (b, h) units (weak scaling: every rank
+runs its own B=8 shard of a global batch of 8N, no collective); decode shards
+the KV sequence (strong scaling) and combines the per-rank (m, l, O) triples
+after one NCCL all-gather (paper_2510_08726_b200.dist).
+
+Timing: W warm-up steps, then exactly K steps between barrier +
+synchronize, CUDA events on the launching stream, max over ranks.  Inputs
+are larger than L2 (126 MB) for every timed workload, so no flush is needed.
+nvidia-smi clocks are sampled during the timed region.
+``--impl reference`` times the fp64 CPU oracle (the reference arm of this
+tier) on a bounded sample of the same workload."""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "attn fwd TFLOP/s & % BF16 peak (seq 4096, d128); decode HBM GB/s; 1/2/4/8 GPU"
+
+WORKLOADS = {
+    # name: (config id, B, Hq, Hkv, S, D, variant)
+    "mha": (2, 8, 16, 16, 4096, 128, dict()),
+    "mha_causal": (2, 8, 16, 16, 4096, 128, dict(causal=True)),
+    "gqa_window": (3, 4, 32, 8, 8192, 128, dict(causal=True, window=(4095, 0))),
+    "var_scaled_dot": (4, 8, 16, 16, 2048, 64, dict()),
+    "var_alibi_causal": (4, 8, 16, 16, 2048, 64, dict(causal=True, alibi=True)),
+    "var_softcap_causal": (4, 8, 16, 16, 2048, 64, dict(causal=True, softcap=50.0)),
+}
+
+
+def allowed_pairs(S: int, variant: dict) -> int:
+    """Number of (query, key) pairs the mask allows for one (b, h), Sq = Skv = S."""
+    causal = variant.get("causal", False)
+    wl, wr = variant.get("window", (-1, -1))
+    total = 0
+    for i in range(S) if (wl >= 0 or wr >= 0) else ():
+        lo = max(0, i - wl) if wl >= 0 else 0
+        hi = min(S - 1, i + wr) if wr >= 0 else S - 1
+        if causal:
+            hi = min(hi, i)
+        total += max(0, hi - lo + 1)
+    if wl >= 0 or wr >= 0:
+        return total
+    return S * (S + 1) // 2 if causal else S * S
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return dict(hbm=float(d["hbm_gbs"]), tf=float(d["bf16_tflops"]),
+                    tf_sustained=float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), src="measured")
+    except Exception:
+        return dict(hbm=6650.0, tf=1590.0, tf_sustained=1400.0, src="fallback")
+
+
+class ClockSampler:
+    """SM clock and clock-event (throttle) reasons sampled every 50 ms during the
+    timed region, through NVML (nvidia-smi's library)."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, gpu_uuid: str):
+        self.uuid, self.samples, self.reasons, self.max_mhz, self.err = gpu_uuid, [], set(), None, None
+        self._stop = threading.Event()
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByUUID(self.uuid.encode() if isinstance(self.uuid, str) else self.uuid)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        except Exception as e:  # noqa: BLE001
+            self.err = f"{type(e).__name__}: {e}"
+            self.t = None
+        return self
+
+    def _run(self):
+        nv = self.nv
+        get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = get_r(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception as e:  # noqa: BLE001
+                self.err = str(e)
+            self._stop.wait(0.05)
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.t:
+            self.t.join(timeout=2)
+        return False
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0,
+                    "error": self.err}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "sm_min_mhz": min(self.samples), "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- reference arm / cpu baseline
+def oracle_sample_rate(name: str, budget_s: float = 15.0, max_heads: int = 64):
+    """fp64 oracle (as it stands) on whole (b, h) heads of the workload: TFLOP/s."""
+    import numpy as np
+
+    import datagen
+    import oracle
+    cid, B, Hq, Hkv, S, D, var = WORKLOADS[name]
+    seed = datagen.config_seed(cid)
+    p = oracle.Problem(B, Hq, Hkv, S, S, D, scale=1.0 / math.sqrt(D), causal=var.get("causal", False),
+                       window_left=var.get("window", (-1, -1))[0], window_right=var.get("window", (-1, -1))[1],
+                       softcap=var.get("softcap", 0.0),
+                       alibi_slopes=datagen.alibi_slopes(Hq) if var.get("alibi") else None)
+    rng = np.random.default_rng(0)
+    flops_head = 4.0 * D * allowed_pairs(S, var)
+    done, t_total = 0, 0.0
+    while done < max_heads and (done == 0 or t_total < budget_s):
+        b, hq = int(rng.integers(B)), int(rng.integers(Hq))
+        g = oracle.head_group(p, hq)
+        qs = datagen.as_f64(datagen.slab(seed, 1, (B, Hq, S, D), b, hq), "bf16")
+        ks = datagen.as_f64(datagen.slab(seed, 2, (B, Hkv, S, D), b, g), "bf16")
+        vs = datagen.as_f64(datagen.slab(seed, 3, (B, Hkv, S, D), b, g), "bf16")
+        t0 = time.perf_counter()
+        oracle.attention_bh(p, qs, ks, vs, hq)
+        t_total += time.perf_counter() - t0
+        done += 1
+    return flops_head * done / t_total / 1e12, done, t_total
+
+
+def blas_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads", 0) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return max(n) if n else os.cpu_count()
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    name = args.workload
+    cid, B, Hq, Hkv, S, D, var = WORKLOADS[name]
+    for _ in range(args.warmup):
+        oracle_sample_rate(name, budget_s=0.0, max_heads=1)
+    rates, times = [], []
+    for _ in range(args.steps):
+        r, n, t = oracle_sample_rate(name, budget_s=0.0, max_heads=1)
+        rates.append(r)
+        times.append(t)
+    value = 4.0 * D * allowed_pairs(S, var) * len(times) / sum(times) / 1e12
+    cores = blas_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(name, args.gpus),
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+                         "sample": f"1 whole (b, h) head of {name} per step ({S}x{S}, D={D}), fp64 numpy oracle"},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(name, n):
+    cid, B, Hq, Hkv, S, D, var = WORKLOADS[name]
+    v = {k: (list(x) if isinstance(x, tuple) else x) for k, x in var.items()}
+    return {"workload": f"{name} (BASELINE config {cid})", "batch_per_gpu": B, "global_batch": B * n,
+            "heads_q": Hq, "heads_kv": Hkv, "seq_len": S, "head_dim": D, "variant": v,
+            "parallelism": f"(b,h)-shard x{n}" if n > 1 else "single GPU",
+            "l2": "inputs larger than L2 (no flush needed)"}
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    import datagen
+    import paper_2510_08726_b200 as pb
+    from datagen import device as dgd
+    from paper_2510_08726_b200 import dist as pdist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    peaks = load_peaks()
+    uuid = str(torch.cuda.get_device_properties(dev).uuid)
+    gpu_id = uuid if uuid.startswith("GPU-") else f"GPU-{uuid}"  # NVML form
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(fn, steps, warmup, sampler=True):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        cs = ClockSampler(gpu_id)
+        with (cs if sampler else _Null()):
+            s0.record()
+            for _ in range(steps):
+                fn()
+            s1.record()
+            torch.cuda.synchronize()
+        barrier()
+        ms = s0.elapsed_time(s1) / steps
+        return max_over_ranks(ms), (cs.summary() if sampler else None)
+
+    # ------------------------------------------------------------- prefill (headline)
+    name = args.workload
+    cid, B, Hq, Hkv, S, D, var = WORKLOADS[name]
+    seed = datagen.config_seed(cid)
+    q = torch.empty(B, Hq, S, D, dtype=torch.bfloat16, device=dev)
+    k = torch.empty(B, Hkv, S, D, dtype=torch.bfloat16, device=dev)
+    v = torch.empty(B, Hkv, S, D, dtype=torch.bfloat16, device=dev)
+    # rank r owns batch rows [rB, (r+1)B) of a global [B*W, ...] tensor (weak scaling)
+    dgd.fill_(q, seed, 1, start=rank * q.numel())
+    dgd.fill_(k, seed, 2, start=rank * k.numel())
+    dgd.fill_(v, seed, 3, start=rank * v.numel())
+    o = torch.empty_like(q)
+    kw = dict(causal=var.get("causal", False), window=var.get("window", (-1, -1)), softcap=var.get("softcap", 0.0))
+    if var.get("alibi"):
+        kw["alibi_slopes"] = torch.tensor(datagen.alibi_slopes(Hq), device=dev)
+    step = lambda: pb.fused_fwd(q, k, v, out=o, **kw)  # noqa: E731
+    step()
+    torch.cuda.synchronize()
+    launches_per_step = pb.last_launch_count()
+    ms, clocks = timed(step, args.steps, args.warmup)
+    flops = 4.0 * D * allowed_pairs(S, var) * B * Hq
+    value = world * flops / (ms * 1e-3) / 1e12
+    achieved = flops / (ms * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(f"fwd_{name}")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded datagen, N(0,1)-like, bf16)",
+        "config": config_dict(name, world), "clocks": clocks,
+        "gpu_launches": launches_per_step * args.steps,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peaks["tf"], "unit": "TFLOP/s",
+                     "frac": achieved / peaks["tf"], "traffic": traffic,
+                     "peak_src": f"{peaks['src']} bf16 burst (MEASURED_PEAKS.json bf16_tflops)",
+                     "kernel": "fwd_tc_kernel (tcgen05 Rolling Update)",
+                     "algorithmic_flops_per_launch": flops},
+    }
+
+    # ------------------------------------------------------------- e2e through the public API, host buffers
+    if not args.no_e2e:
+        hq_, hk_, hv_ = (t.cpu().pin_memory() for t in (q, k, v))
+        ho_ = torch.empty(o.shape, dtype=o.dtype).pin_memory()
+        e2e_steps = max(1, min(args.steps, 5))
+
+        def e2e_step():
+            return pb.fused_fwd(hq_, hk_, hv_, out=ho_, **kw)
+        ms_e2e, _ = timed(e2e_step, e2e_steps, 1, sampler=False)
+        line["e2e"] = {"value": world * flops / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOP/s",
+                       "h2d_bytes_per_step": 3 * q.numel() * 2, "d2h_bytes_per_step": o.numel() * 2,
+                       "ms_per_step": ms_e2e, "steps": e2e_steps}
+        del hq_, hk_, hv_, ho_
+
+    del q, k, v, o
+    torch.cuda.empty_cache()
+
+    # ------------------------------------------------------------- decode (secondary metric)
+    if not args.no_decode:
+        Bd, Hqd, Hkvd, L, Dd = args.decode_batch, 32, 8, 131072, 128
+        seed5 = datagen.config_seed(5)
+        lo, hi = pdist.shard_range(L, rank, world)
+        qd = torch.empty(Bd, Hqd, 1, Dd, dtype=torch.bfloat16, device=dev)
+        dgd.fill_(qd, seed5, 1)
+        kd = torch.empty(Bd, Hkvd, hi - lo, Dd, dtype=torch.bfloat16, device=dev)
+        vd = torch.empty_like(kd)
+        for b in range(Bd):
+            for h in range(Hkvd):
+                start = ((b * Hkvd + h) * L + lo) * Dd
+                dgd.fill_(kd[b, h], seed5, 2, start=start)
+                dgd.fill_(vd[b, h], seed5, 3, start=start)
+        od = torch.empty_like(qd)
+        ws = torch.empty(pb.workspace_bytes(qd, kd), dtype=torch.uint8, device=dev)
+        if world == 1:
+            dstep = lambda: pb.splitkv_decode(qd, kd, vd, causal=True, out=od, workspace=ws)  # noqa: E731
+        else:
+            dstep = lambda: pdist.decode_kv_sharded(qd, kd, vd, kv_pos_offset=lo, seqlen_kv_total=L,  # noqa: E731
+                                                    causal=True)
+        dstep()
+        torch.cuda.synchronize()
+        dl = pb.last_launch_count()
+        dms, dclk = timed(dstep, args.steps, args.warmup)
+        kv_bytes = 2.0 * Bd * Hkvd * L * Dd * 2
+        gbs = kv_bytes / (dms * 1e-3) / 1e9
+        per_rank = kv_bytes / world / (dms * 1e-3) / 1e9
+        line["decode"] = {
+            "metric": "split-KV decode HBM GB/s (K+V bytes read once / time)", "value": gbs, "unit": "GB/s",
+            "ms_per_step": dms, "scaling": "strong" if world > 1 else None, "clocks": dclk,
+            "config": {"workload": "decode (BASELINE config 5)", "batch": Bd, "heads_q": Hqd, "heads_kv": Hkvd,
+                       "kv_len": L, "head_dim": Dd, "causal": True,
+                       "parallelism": f"KV-sequence shard x{world} + NCCL all-gather of (m,l,O)" if world > 1
+                       else "single GPU split-KV", "l2": "KV larger than L2"},
+            "gpu_launches_per_step": dl,
+            "roofline": {"bound": "hbm", "achieved": per_rank, "peak": peaks["hbm"], "unit": "GB/s",
+                         "frac": per_rank / peaks["hbm"], "traffic": None,
+                         "peak_src": f"{peaks['src']} hbm_gbs (copy)", "kernel": "decode_split_kernel + combine"},
+        }
+        del qd, kd, vd, od, ws
+
+    # ------------------------------------------------------------- CPU baseline (oracle), rank 0, N = 1
+    if rank == 0 and world == 1 and not args.no_cpu:
+        rate, heads, secs = oracle_sample_rate(name, budget_s=args.cpu_budget)
+        line["cpu_baseline"] = {"value": rate, "unit": "TFLOP/s", "cores": blas_threads(), "kind": "oracle",
+                                "sample": f"{heads} whole (b,h) heads of {name} ({S}x{S}, D={D}) in {secs:.1f} s, "
+                                          "fp64 numpy oracle (oracle.attention_bh)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=list(WORKLOADS), default="mha")
+    ap.add_argument("--decode-batch", type=int, default=16)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        main_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,74 @@
+"""Multi-GPU partitioning of the hot path (one process per GPU, torch.distributed).
+
+* Prefill (Rolling Update) shards independent (b, h) units: nothing is
+  exchanged (``shard_range``).
+* Long-context decode shards the KV sequence (``decode_kv_sharded``): each
+  rank runs the Split-K local section over its keys
+  [r L / W, (r + 1) L / W) with ``kv_pos_offset`` set to the shard start,
+  merges its splits into ONE un-normalised (m, l, O) triple per (b, h)
+  (Eq. 8 without the divide), all-gathers the packed [B, H, D + 2] fp32
+  triples (the only collective on the path), and applies the Eq. 8 combine
+  over the W parts.  Exact because h commutes with the reducer (Eq. 4,
+  P:578-579), so the merge may be grouped by split and then by rank.
+
+The local section and the combine are injectable so the host-side logic can
+be tested on CPU with world_size 2 over gloo; the defaults are the CUDA
+kernels behind the C ABI.
+"""
+from __future__ import annotations
+
+from typing import Callable, Optional
+
+import torch
+import torch.distributed as dist
+
+from . import Parts, combine, splitkv_decode
+
+
+def shard_range(n: int, rank: int, world: int):
+    """Contiguous, balanced [lo, hi) of n units for `rank` (first n % W ranks get one more)."""
+    base, extra = divmod(n, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def _local_kernels(q, k_shard, v_shard, *, kv_pos_offset, seqlen_kv_total, num_splits, variant):
+    B, Hq, _, D = q.shape
+    splits = num_splits
+    if splits == 0:
+        from . import default_splits
+        splits = default_splits(q, k_shard)
+    parts = Parts.empty(splits, B, Hq, D, q.device)
+    splitkv_decode(q, k_shard, v_shard, num_splits=splits, parts=parts, want_out=False,
+                   kv_pos_offset=kv_pos_offset, seqlen_kv_total=seqlen_kv_total, **variant)
+    return parts
+
+
+def _merge_kernels(parts: Parts, acc: Parts):
+    combine(parts, acc=acc, want_out=False)
+
+
+def _final_kernels(parts: Parts, out_dtype, return_lse):
+    return combine(parts, out_dtype=out_dtype, return_lse=return_lse)
+
+
+def decode_kv_sharded(q: torch.Tensor, k_shard: torch.Tensor, v_shard: torch.Tensor, *, kv_pos_offset: int,
+                      seqlen_kv_total: int, group=None, num_splits: int = 0, return_lse: bool = False,
+                      local: Optional[Callable] = None, merge: Optional[Callable] = None,
+                      final: Optional[Callable] = None, **variant):
+    """KV-sequence-sharded Split-K decode. q [B, Hq, 1, D] is replicated;
+    k_shard/v_shard [B, Hkv, L_r, D] hold keys [kv_pos_offset, kv_pos_offset + L_r)
+    of a sequence of seqlen_kv_total keys.  Returns O [B, Hq, 1, D] (and lse)
+    on every rank."""
+    local = local or _local_kernels
+    merge = merge or _merge_kernels
+    final = final or _final_kernels
+    world = dist.get_world_size(group)
+    B, Hq, _, D = q.shape
+    parts = local(q, k_shard, v_shard, kv_pos_offset=kv_pos_offset, seqlen_kv_total=seqlen_kv_total,
+                  num_splits=num_splits, variant=variant)
+    send = torch.empty(1, B, Hq, D + 2, dtype=torch.float32, device=q.device)
+    merge(parts, Parts.packed(send))
+    recv = torch.empty(world, B, Hq, D + 2, dtype=torch.float32, device=q.device)
+    dist.all_gather_into_tensor(recv, send, group=group)
+    return final(Parts.packed(recv), q.dtype, return_lse)
