@@ -75,7 +75,7 @@ def load_peaks():
 
 
 class ClockSampler:
-    """SM clock and clock-event (throttle) reasons sampled every 50 ms during the
+    """SM clock and clock-event (throttle) reasons sampled every 10 ms during the
     timed region, through NVML (nvidia-smi's library)."""
 
     REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
@@ -111,7 +111,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception as e:  # noqa: BLE001
                 self.err = str(e)
-            self._stop.wait(0.05)
+            self._stop.wait(0.01)
 
     def __exit__(self, *a):
         self._stop.set()
@@ -376,7 +376,7 @@ class _Null:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=list(WORKLOADS), default="mha")

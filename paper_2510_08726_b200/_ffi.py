@@ -6,7 +6,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libattn.so")
+# ATTN_LIB_PATH overrides the in-tree library (developer A/B builds only).
+LIB_PATH = os.environ.get("ATTN_LIB_PATH") or os.path.join(_HERE, "libattn.so")
 
 ATTN_OK = 0
 ATTN_ERR_INVALID_ARGUMENT = 1

@@ -10,11 +10,14 @@
 //
 // B200 mapping:
 //   CTA = 2 query tiles of BM = 128 rows of one (b, hq) -> 256 rows; 384 threads.
-//   warp 0      : TMA producer (Q once; K_j / V_j through a ring of kStages slots)
-//   warp 1      : tcgen05.mma issuer (one thread)
-//   warp 2      : TMEM allocator (512 columns)
-//   warps 4-7   : softmax/correction/epilogue for query tile 0 (thread = row)
-//   warps 8-11  : same for query tile 1
+//   warps 0-3   : softmax/correction/epilogue for query tile 0 (thread = row)
+//   warps 4-7   : same for query tile 1
+//   warp 8      : TMA producer (Q once; K_j / V_j through a ring of kStages slots,
+//                 plus L2 prefetch kPrefetch tiles ahead)
+//   warp 9      : tcgen05.mma issuer (one thread)
+//   warp 10     : TMEM allocator (512 columns)
+//   The producer and MMA warps get the HIGHEST warp ids on purpose: the warp
+//   arbiter is highest-id-first, so they are never starved by the softmax warps.
 //   TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512) (fp32 columns);
 //         P_t (bf16) overwrites the first 64 columns of S_t and feeds the
 //         PV MMA straight from TMEM (A operand in TMEM).
@@ -34,20 +37,59 @@ namespace {
 constexpr int BM = 128;
 constexpr int BN = 128;
 constexpr int kThreads = 384;
+constexpr int kWarpLoad = 8, kWarpMma = 9, kWarpAlloc = 10;
+#ifndef ATTN_PREFETCH
+#define ATTN_PREFETCH 0
+#endif
+constexpr int kPrefetch = ATTN_PREFETCH;   // KV tiles prefetched into L2 ahead of the TMA loads
 constexpr float kTau = 8.0f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kLog2e = 1.4426950408889634f;
+constexpr uint32_t kBarTok0 = 3, kBarTok1 = 4;   // named barriers of the exp token
+#ifndef ATTN_TOKEN
+#define ATTN_TOKEN 0
+#endif
+constexpr bool kToken = ATTN_TOKEN != 0;   // alternate the two softmax warpgroups' exp phases
+
+#ifndef ATTN_SLEEP_WAIT
+#define WAIT_LM(bar, par) mbar_wait_spin(bar, par)   // loader / MMA thread waits: poll
+#else
+#define WAIT_LM(bar, par) mbar_wait(bar, par)
+#endif
+
+#ifdef ATTN_TRACE
+// Debug-only timeline of one CTA: clock64() per (event, step), kept in shared
+// memory while the kernel runs (so tracing adds no global-memory traffic
+// before the mbarrier releases) and copied to g_trace at the end.
+constexpr int kTrEv = 26, kTrSteps = 40;
+__device__ long long g_trace[kTrEv][kTrSteps];
+__device__ __forceinline__ bool trace_cta() { return blockIdx.x == 5 && blockIdx.y == 3 && blockIdx.z == 2; }
+#define TRACE(ev, step)                                                          \
+  do {                                                                           \
+    if (trace_cta() && (step) < kTrSteps) s_trace[(ev) * kTrSteps + (step)] = clock64(); \
+  } while (0)
+#else
+#define TRACE(ev, step) do { } while (0)
+#endif
 
 template <int D>
 struct Cfg {
   static constexpr int kBoxes = D / 64;           // 64-column (128 B) swizzle atoms per row
   static constexpr int kQTileBytes = BM * D * 2;
   static constexpr int kKVTileBytes = BN * D * 2;
-  static constexpr int kStages = (D == 128) ? 4 : 8;
+#ifdef ATTN_TRACE
+  static constexpr int kStages = (D == 128) ? 4 : 8;   // room for the shared-memory trace
+#else
+  static constexpr int kStages = (D == 128) ? 5 : 10;
+#endif
   static constexpr int kSmemQ = 2 * kQTileBytes;
   static constexpr int kSmemKV = kStages * kKVTileBytes;
   static constexpr int kNumBars = 1 + 2 * kStages + 6;
+#ifdef ATTN_TRACE
+  static constexpr int kSmemBytes = 1024 + kSmemQ + kSmemKV + 1024 + 26 * 40 * 8;
+#else
   static constexpr int kSmemBytes = 1024 + kSmemQ + kSmemKV + kNumBars * 8 + 16;
+#endif
 };
 
 struct Range {
@@ -84,6 +126,25 @@ __device__ __forceinline__ Range tile_range(const Shape& s, const VariantParams&
   return r;
 }
 
+// 2^x on the FMA/ALU pipes (FA4-style MUFU offload): round-to-nearest split
+// x = k + f, f in [-1/2, 1/2]; degree-3 minimax polynomial for 2^f (relative
+// error 7.5e-5, below bf16's 2^-9 half-ulp of P); 2^k added to the exponent
+// bits.  Exact 0 for x < -126 (masked / -inf inputs).
+__device__ __forceinline__ float ex2_poly(float x) {
+  const float xc = fmaxf(x, -127.f);
+  const float t = xc + 12582912.f;            // 1.5 * 2^23: low mantissa bits = round(x)
+  const float f = xc - (t - 12582912.f);
+  float p = fmaf(0.05517109f, f, 0.24261115f);
+  p = fmaf(p, f, 0.6932611f);
+  p = fmaf(p, f, 0.99992806f);
+  const float r = __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+  return x < -126.f ? 0.f : r;
+}
+
+#ifndef ATTN_POLY_DIV
+#define ATTN_POLY_DIV 0   // every ATTN_POLY_DIV-th pair of exponentials uses ex2_poly (0 = none)
+#endif
+
 __device__ __forceinline__ bool active(const Range& r, int j) { return j >= r.lo && j < r.hi; }
 
 __device__ __forceinline__ float u2f(uint32_t u) { return __uint_as_float(u); }
@@ -105,7 +166,7 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
 template <bool kAlibi, bool kSoftcap, bool kMask>
 __device__ __forceinline__ float score_tile(float (&x)[BN], const VariantParams& v, float nslope2, float dq0,
                                             int rel_lo, int rel_hi) {
-  float mt = -INFINITY;
+  float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};   // independent chains for ILP
 #pragma unroll
   for (int c = 0; c < BN; ++c) {
     float xv = x[c];
@@ -117,8 +178,9 @@ __device__ __forceinline__ float score_tile(float (&x)[BN], const VariantParams&
     if constexpr (kAlibi) xv = fmaf(nslope2, fabsf(dq0 - (float)c), xv);  // R4: -slope |qpos - kpos|
     if constexpr (kMask) xv = (c >= rel_lo && c <= rel_hi) ? xv : -INFINITY;
     x[c] = xv;
-    mt = fmaxf(mt, xv);
+    mx[c & 3] = fmaxf(mx[c & 3], xv);
   }
+  float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
   if constexpr (!kAlibi && !kSoftcap) mt *= v.scale_log2;
   return mt;
 }
@@ -142,6 +204,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* p_ready = s_full + 2;
   uint64_t* o_done = p_ready + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+#ifdef ATTN_TRACE
+  long long* s_trace = reinterpret_cast<long long*>(smem + C::kSmemQ + C::kSmemKV + 1024);
+  if (trace_cta())
+    for (int i = threadIdx.x; i < kTrEv * kTrSteps; i += blockDim.x) s_trace[i] = 0;
+#endif
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int qblk = v.causal ? (int)(gridDim.x - 1 - blockIdx.x) : (int)blockIdx.x;  // heavy causal tiles first
@@ -160,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ulo = rng1.lo; uhi = rng1.hi;
   }
 
-  if (warp == 0 && lane == 0) {
+  if (warp == kWarpLoad && lane == 0) {
     prefetch_tmap(&tm_q);
     prefetch_tmap(&tm_k);
     prefetch_tmap(&tm_v);
@@ -177,27 +244,44 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     fence_mbarrier_init();
   }
-  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  if (warp == kWarpAlloc) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) TRACE(3, 0);
 
-  if (warp == 0) {
+  if (warp == kWarpLoad) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       const uint64_t pol_q = policy_evict_first();
+#ifdef ATTN_KV_EVICT_NORMAL
+      const uint64_t pol_kv = policy_evict_normal();
+#else
       const uint64_t pol_kv = policy_evict_last();   // K/V are re-read by the other q-blocks of this head
+#endif
       const int nq = has_rows1 ? 2 : 1;
       mbar_arrive_expect_tx(q_full, nq * C::kQTileBytes);
       for (int t = 0; t < nq; ++t)
         for (int bx = 0; bx < C::kBoxes; ++bx)
           tma_load_4d(&tm_q, q_full, sQ + t * C::kQTileBytes + bx * BM * 128, bx * 64, row0 + t * BM, hq, b, pol_q);
+      if (kPrefetch > 0)
+      for (int j = ulo; j < min(ulo + kPrefetch, uhi); ++j)
+        for (int bx = 0; bx < C::kBoxes; ++bx) {
+          tma_prefetch_4d(&tm_k, bx * 64, j * BN, hkv, b);
+          tma_prefetch_4d(&tm_v, bx * 64, j * BN, hkv, b);
+        }
       int it = 0;
       for (int j = ulo; j < uhi; ++j) {
+        if (kPrefetch > 0 && j + kPrefetch < uhi)
+          for (int bx = 0; bx < C::kBoxes; ++bx) {
+            tma_prefetch_4d(&tm_k, bx * 64, (j + kPrefetch) * BN, hkv, b);
+            tma_prefetch_4d(&tm_v, bx * 64, (j + kPrefetch) * BN, hkv, b);
+          }
         for (int kind = 0; kind < 2; ++kind, ++it) {
           const int slot = it % C::kStages;
-          mbar_wait(&kv_empty[slot], ((it / C::kStages) & 1) ^ 1);
+          WAIT_LM(&kv_empty[slot], ((it / C::kStages) & 1) ^ 1);
+          TRACE(24 + kind, j);
           mbar_arrive_expect_tx(&kv_full[slot], C::kKVTileBytes);
           uint8_t* dst = sKV + slot * C::kKVTileBytes;
           const CUtensorMap* tm = kind == 0 ? &tm_k : &tm_v;
@@ -206,8 +290,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
+  } else if (warp == kWarpMma) {
+    // ------------------------------------------------------------ MMA issuer (one thread)
     if (lane == 0 && uhi > ulo) {
       constexpr uint32_t idesc_qk = idesc_bf16_f32(BM, BN, 0, 0);  // Q K-major, K K-major
       constexpr uint32_t idesc_pv = idesc_bf16_f32(BM, D, 0, 1);   // P (TMEM), V MN-major
@@ -215,13 +299,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t tO[2] = {tmem + 256, tmem + 384};
       const Range rg[2] = {rng0, rng1};
       uint32_t p_phase[2] = {0, 0};
-      mbar_wait(q_full, 0);
+      WAIT_LM(q_full, 0);
 
       auto wait_slot = [&](int it) {
-        mbar_wait(&kv_full[it % C::kStages], (it / C::kStages) & 1);
+        WAIT_LM(&kv_full[it % C::kStages], (it / C::kStages) & 1);
         tc_fence_after();
       };
-      auto qk = [&](int t, int it) {
+      auto qk = [&](int t, int it) {   // S_t = Q_t K^T
         const uint32_t sq = smem_u32(sQ + t * C::kQTileBytes);
         const uint32_t sk = smem_u32(sKV + (it % C::kStages) * C::kKVTileBytes);
 #pragma unroll
@@ -233,10 +317,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mma_commit(&s_full[t]);
       };
-      auto pv = [&](int t, int it, bool acc) {
-        mbar_wait(&p_ready[t], p_phase[t]);
+      auto pv = [&](int t, int it, bool acc) {   // O_t += P_t V (P straight from TMEM)
+        WAIT_LM(&p_ready[t], p_phase[t]);
         p_phase[t] ^= 1;
         tc_fence_after();
+        TRACE(13 + t, it / 2);
         const uint32_t sv = smem_u32(sKV + (it % C::kStages) * C::kKVTileBytes);
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk)
@@ -253,12 +338,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int itV = 2 * (j - ulo) + 1, itK1 = itV + 1;
         const bool more = j + 1 < uhi;
         wait_slot(itV);
+        TRACE(12, j);
         if (active(rg[0], j)) pv(0, itV, j > rg[0].lo);
+        TRACE(0, j);
         if (more) {
           wait_slot(itK1);
+          TRACE(15, j);
           if (active(rg[0], j + 1)) qk(0, itK1);
         }
+        TRACE(1, j);
         if (active(rg[1], j)) pv(1, itV, j > rg[1].lo);
+        TRACE(2, j);
         mma_commit(&kv_empty[itV % C::kStages]);
         if (more) {
           if (active(rg[1], j + 1)) qk(1, itK1);
@@ -266,9 +356,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp < 8) {
     // ------------------------------------------------------------ softmax / correction / epilogue
-    const int t = (int)(warp - 4) >> 2;
+    const int t = (int)warp >> 2;
     const int wq = warp & 3;
     const int r = wq * 32 + lane;
     const Range R = t == 0 ? rng0 : rng1;
@@ -283,10 +373,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     float m_ref = -INFINITY;  // stale reference max (log2 units), R9
     float l = 0.f;            // running denominator (sum of un-rounded fp32 p, R10)
 
-    for (int j = R.lo; j < R.hi; ++j) {
+    // Ping-pong: the exp phases of the two warpgroups alternate in KV-tile order
+    // (token passed through named barriers 3/4), so one tile's softmax always
+    // runs under the other tile's MMAs instead of both contending for MUFU.
+    if (kToken && t == 1 && uhi > ulo) named_bar_arrive(kBarTok0, 256);
+    for (int j = ulo; j < uhi; ++j) {
+      if (!active(R, j)) {   // keep the token moving through tiles this warpgroup skips
+        if (!kToken) continue;
+        named_bar_sync(t == 0 ? kBarTok0 : kBarTok1, 256);
+        if (t == 0) named_bar_arrive(kBarTok1, 256);
+        else if (j + 1 < uhi) named_bar_arrive(kBarTok0, 256);
+        continue;
+      }
       const int it = j - R.lo;
+      if (wq == 0 && lane == 0) TRACE(4 + 4 * t, j);
       mbar_wait(&s_full[t], it & 1);
       tc_fence_after();
+      if (wq == 0 && lane == 0) TRACE(5 + 4 * t, j);
       float x[BN];
       {
         uint32_t u[BN];
@@ -317,25 +420,43 @@ __global__ void __launch_bounds__(kThreads, 1)
       l *= alpha;                                       // xsum = h(xsum) + ...
       // exp(x - m), local sum, P -> bf16 into TMEM (aliasing S)
       const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
-      float sum = 0.f;
+      if (kToken) named_bar_sync(t == 0 ? kBarTok0 : kBarTok1, 256);   // acquire the exp token
+      if (wq == 0 && lane == 0) TRACE(6 + 4 * t, j);
+      float sum0 = 0.f, sum1 = 0.f;
 #pragma unroll
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t pk[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          float p0, p1;
+          float a0, a1;
           if constexpr (kPlain) {
-            p0 = ex2_approx(fmaf(x[c0 + 2 * e], v.scale_log2, -m_use));
-            p1 = ex2_approx(fmaf(x[c0 + 2 * e + 1], v.scale_log2, -m_use));
+            a0 = fmaf(x[c0 + 2 * e], v.scale_log2, -m_use);
+            a1 = fmaf(x[c0 + 2 * e + 1], v.scale_log2, -m_use);
           } else {
-            p0 = ex2_approx(x[c0 + 2 * e] - m_use);
-            p1 = ex2_approx(x[c0 + 2 * e + 1] - m_use);
+            a0 = x[c0 + 2 * e] - m_use;
+            a1 = x[c0 + 2 * e + 1] - m_use;
           }
-          sum += p0 + p1;
+          float p0, p1;
+          if (ATTN_POLY_DIV > 0 && (e % (ATTN_POLY_DIV > 0 ? ATTN_POLY_DIV : 1)) == (ATTN_POLY_DIV > 0 ? ATTN_POLY_DIV : 1) - 1) {
+            p0 = ex2_poly(a0);
+            p1 = ex2_poly(a1);
+          } else {
+            p0 = ex2_approx(a0);
+            p1 = ex2_approx(a1);
+          }
+          sum0 += p0;
+          sum1 += p1;
           pk[e] = pack_bf16x2(p0, p1);
         }
         tmem_st16(tS + c0 / 2, pk);
       }
+      if (kToken) {                                         // release the token
+        if (t == 0) named_bar_arrive(kBarTok1, 256);
+        else if (j + 1 < uhi) named_bar_arrive(kBarTok0, 256);
+      }
+      const float sum = sum0 + sum1;
+      if (wq == 0 && lane == 0) TRACE(7 + 4 * t, j);
+      if (t == 0 && lane == 0) TRACE(16 + wq, j);
       // (done after P so the S registers are dead; PV(j) cannot start before p_ready)
       if (__any_sync(0xffffffffu, need_o)) {
         // O = h(O): wait for PV of the previous tile, then rescale the TMEM accumulator.
@@ -356,6 +477,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       l += sum;
       tc_fence_before();
       __syncwarp();
+      if (t == 0 && lane == 0) TRACE(20 + wq, j);
       if (lane == 0) mbar_arrive(&p_ready[t]);
     }
 
@@ -406,7 +528,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+#ifdef ATTN_TRACE
+  if (trace_cta())
+    for (int i = threadIdx.x; i < kTrEv * kTrSteps; i += blockDim.x) (&g_trace[0][0])[i] = s_trace[i];
+#endif
+  if (warp == kWarpAlloc) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
@@ -433,6 +559,12 @@ cudaError_t launch_d(const FwdTcArgs& a, cudaStream_t stream) {
 }
 
 }  // namespace
+
+#ifdef ATTN_TRACE
+extern "C" __attribute__((visibility("default"))) int attn_debug_trace(long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(g_trace));
+}
+#endif
 
 cudaError_t launch_fwd_tc(const FwdTcArgs& a, cudaStream_t stream, int* launches) {
   cudaError_t e = a.s.D == 128 ? launch_d<128>(a, stream) : launch_d<64>(a, stream);

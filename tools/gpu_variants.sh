@@ -1,0 +1,15 @@
+#!/bin/bash
+# Bench every build/var_*/libattn.so on the given workloads.
+cd "$GRAFT_REPO_ROOT"
+OUT=gpurun_out/variants_${1:-x}.log; : > $OUT
+for lib in build/var_*/libattn.so; do
+  for w in ${WORKLOADS:-mha mha_causal}; do
+    ATTN_LIB_PATH=$PWD/$lib timeout 300 python bench.py --steps 20 --warmup 5 --no-e2e --no-decode --no-cpu --workload $w 2>&1 | \
+      python -c "import sys,json
+for l in sys.stdin:
+    try: d=json.loads(l)
+    except Exception: print(l.rstrip()[:200]); continue
+    print('$lib $w', round(d['value'],1), 'frac', round(d['roofline']['frac'],3), 'clk', d['clocks'].get('sm_mhz'))" >> $OUT
+  done
+done
+cat $OUT

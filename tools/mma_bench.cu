@@ -1,0 +1,128 @@
+// mma_bench.cu -- isolated tcgen05.mma throughput on one CTA per SM (148 CTAs):
+// cycles per kind::f16 MMA (bf16, fp32 accumulate) for the shapes the
+// attention kernel issues.  Operands are whatever is in shared memory / TMEM
+// (throughput only).  Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3
+// -std=c++17 -I paper_2510_08726_b200/csrc tools/mma_bench.cu -o build/mma_bench
+#include <cstdio>
+#include <vector>
+
+#include "ptx.cuh"
+
+using namespace attn;
+
+template <int N, bool kTS, int kAccum, int kLd, int kCopy = 0>
+__global__ void __launch_bounds__(256, 1) bench(long long* out, int iters, const uint8_t* gsrc) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x / 32;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbarrier_init();
+  }
+  if (warp == 0) tmem_alloc<512>(&tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  __shared__ volatile int done;
+  if (threadIdx.x == 0) done = 0;
+  __syncthreads();
+  if (kLd && warp >= 4) {
+    // TMEM readers (like softmax warps): 32x32b.x32 loads of columns [256, 384) until the MMAs finish
+    uint32_t r[32];
+    const uint32_t base = tmem + 256 + ((uint32_t)((warp & 3) * 32) << 16);
+    float acc = 0.f;
+    while (!done) {
+      for (int c = 0; c < kLd; ++c) {
+        tmem_ld32(base + (c & 3) * 32, r);
+        tmem_ld_wait();
+        acc += __uint_as_float(r[0]) + __uint_as_float(r[31]);
+      }
+    }
+    if (acc == 12345.f) out[0] = 1;
+  }
+  __shared__ uint64_t cbar;
+  __shared__ long long copy_bytes;
+  if (kCopy && threadIdx.x == 32) {
+    // bulk copies global -> shared (like TMA K/V loads) into [64 KB, 96 KB) until the MMAs finish
+    mbar_init(&cbar, 1);
+    fence_mbarrier_init();
+    long long bytes = 0;
+    uint32_t ph = 0;
+    const uint8_t* src = gsrc + blockIdx.x * (1 << 20);
+    while (!done) {
+      mbar_arrive_expect_tx(&cbar, 32768);
+      bulk_load_1d(smem + 65536, src + (bytes & ((1 << 20) - 1)), 32768, &cbar, policy_evict_normal());
+      mbar_wait_spin(&cbar, ph);
+      ph ^= 1;
+      bytes += 32768;
+    }
+    copy_bytes = bytes;
+  }
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = idesc_bf16_f32(128, N, 0, kTS ? 1 : 0);
+    const uint32_t sa = smem_u32(smem), sb = smem_u32(smem + 32768);
+    long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const uint32_t d = tmem + (kAccum > 1 ? (i % kAccum) * N : 0);
+        if constexpr (kTS)
+          mma_ts(d, tmem + 384 + kk * 8, smem_desc_sw128(sb + kk * 2048, 16384, 1024), idesc, 1);
+        else
+          mma_ss(d, smem_desc_sw128(sa + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                 smem_desc_sw128(sb + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024), idesc, 1);
+      }
+    }
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    out[blockIdx.x] = t1 - t0;
+    done = 1;
+  }
+  __syncthreads();
+  if (kCopy && threadIdx.x == 0) out[148 + blockIdx.x] = copy_bytes;
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+template <int N, bool kTS, int kAccum, int kLd = 0, int kCopy = 0>
+void run(const char* name, long long* d_out) {
+  const int iters = 2000;
+  auto k = bench<N, kTS, kAccum, kLd, kCopy>;
+  static uint8_t* g = nullptr;
+  if (!g) cudaMalloc(&g, 148u << 20);
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+  k<<<148, 256, 96 * 1024>>>(d_out, 10, g);
+  k<<<148, 256, 96 * 1024>>>(d_out, iters, g);
+  cudaError_t e = cudaDeviceSynchronize();
+  std::vector<long long> h(296);
+  cudaMemcpy(h.data(), d_out, 296 * 8, cudaMemcpyDeviceToHost);
+  double avg = 0, cb = 0;
+  for (int i = 0; i < 148; ++i) { avg += h[i]; cb += h[148 + i]; }
+  avg /= 148; cb /= 148;
+  if (kCopy) printf("   copy: %.1f B/clk per SM during the MMAs\n", cb / avg);
+  const double mmas = iters * 8.0;
+  printf("%-28s %s  cycles/MMA %.1f  (ideal %.0f)  flop/clk/SM %.0f\n", name, cudaGetErrorString(e), avg / mmas,
+         128.0 * N / 256.0, 2.0 * 128 * N * 16 * mmas / avg);
+}
+
+int main() {
+  long long* d;
+  cudaMalloc(&d, 296 * 8);
+  run<128, false, 1>("SS M128 N128 K16", d);
+  run<256, false, 1>("SS M128 N256 K16", d);
+  run<128, true, 1>("TS M128 N128 K16 (A tmem)", d);
+  run<128, false, 2>("SS N128 2 accumulators", d);
+  run<64, false, 1>("SS M128 N64 K16", d);
+  run<128, false, 1, 1>("SS N128 + 4 LDTM warps", d);
+  run<128, true, 1, 1>("TS N128 + 4 LDTM warps", d);
+  run<128, false, 1, 0, 1>("SS N128 + bulk copies", d);
+  run<128, true, 1, 0, 1>("TS N128 + bulk copies", d);
+  return 0;
+}

@@ -1,0 +1,29 @@
+"""Build build/libattn_trace.so (-DATTN_TRACE) and print a per-step timeline of one CTA of the MHA config."""
+import ctypes, os, subprocess, sys
+import numpy as np
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+lib_path = os.path.join(ROOT, "build", "libattn_trace.so")
+if not os.path.exists(lib_path):
+    src = [os.path.join(ROOT, "paper_2510_08726_b200", "csrc", f) for f in ("api.cu", "fwd_tc.cu", "fwd_simt.cu", "decode.cu")]
+    subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+                           "-Xcompiler", "-fPIC", "-DATTN_TRACE", "-shared", "-o", lib_path] + src)
+import torch
+from paper_2510_08726_b200 import _ffi
+_ffi.load(lib_path)
+import paper_2510_08726_b200 as pb
+from datagen import device as dgd
+B, H, S, D = 8, 16, 4096, 128
+q, k, v = (dgd.tensor(1, i, (B, H, S, D)) for i in (1, 2, 3))
+causal = len(sys.argv) > 1 and sys.argv[1] == "causal"
+for _ in range(3):
+    o = pb.fused_fwd(q, k, v, causal=causal)
+torch.cuda.synchronize()
+tr = np.zeros((26, 40), dtype=np.int64)
+ctypes.CDLL(lib_path).attn_debug_trace(tr.ctypes.data_as(ctypes.c_void_p))
+t0 = tr[3, 0]
+names = {12: "mma:V ready", 13: "mma:P0 seen", 15: "mma:K+1 ready", 14: "mma:P1 seen", 0: "mma:PV0 iss", 1: "mma:QK0+1 iss", 2: "mma:PV1 iss", 4: "sm0:wait S", 5: "sm0:S ready",
+         6: "sm0:token", 7: "sm0:P done", 8: "sm1:wait S", 9: "sm1:S ready", 10: "sm1:token", 11: "sm1:P done", 16: "w4 exp end", 17: "w5 exp end", 18: "w6 exp end", 19: "w7 exp end", 20: "w4 arrive", 21: "w5 arrive", 22: "w6 arrive", 23: "w7 arrive", 24: "ld:K issue", 25: "ld:V issue"}
+print("step " + " ".join(f"{names[e]:>13s}" for e in names))
+for j in range(33):
+    print(f"{j:4d} " + " ".join(f"{(tr[e, j] - t0) if tr[e, j] else 0:13d}" for e in names))
