@@ -47,7 +47,7 @@ constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr uint32_t kBarTok0 = 3, kBarTok1 = 4;   // named barriers of the exp token
 #ifndef ATTN_TOKEN
-#define ATTN_TOKEN 0
+#define ATTN_TOKEN 1
 #endif
 constexpr bool kToken = ATTN_TOKEN != 0;   // alternate the two softmax warpgroups' exp phases
 
@@ -291,8 +291,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == kWarpMma) {
-    // ------------------------------------------------------------ MMA issuer (one thread)
-    if (lane == 0 && uhi > ulo) {
+    // ------------------------------------------------------------ MMA issuer
+    // The whole warp runs this role with warp-uniform values; one elected lane
+    // issues each tcgen05 instruction (see mma_*_warp).
+    if (uhi > ulo) {
       constexpr uint32_t idesc_qk = idesc_bf16_f32(BM, BN, 0, 0);  // Q K-major, K K-major
       constexpr uint32_t idesc_pv = idesc_bf16_f32(BM, D, 0, 1);   // P (TMEM), V MN-major
       const uint32_t tS[2] = {tmem, tmem + 128};
@@ -312,47 +314,47 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t ka = (kk >> 2) * (BM * 128) + (kk & 3) * 32;
           const uint32_t kb = (kk >> 2) * (BN * 128) + (kk & 3) * 32;
-          mma_ss(tS[t], smem_desc_sw128(sq + ka, 16, 1024), smem_desc_sw128(sk + kb, 16, 1024), idesc_qk,
+          mma_ss_warp(tS[t], smem_desc_sw128(sq + ka, 16, 1024), smem_desc_sw128(sk + kb, 16, 1024), idesc_qk,
                  kk > 0 ? 1u : 0u);
         }
-        mma_commit(&s_full[t]);
+        mma_commit_warp(&s_full[t]);
       };
       auto pv = [&](int t, int it, bool acc) {   // O_t += P_t V (P straight from TMEM)
         WAIT_LM(&p_ready[t], p_phase[t]);
         p_phase[t] ^= 1;
         tc_fence_after();
-        TRACE(13 + t, it / 2);
+        if (lane == 0) TRACE(13 + t, it / 2);
         const uint32_t sv = smem_u32(sKV + (it % C::kStages) * C::kKVTileBytes);
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk)
-          mma_ts(tO[t], tS[t] + kk * 8, smem_desc_sw128(sv + kk * 2048, BN * 128, 1024), idesc_pv,
+          mma_ts_warp(tO[t], tS[t] + kk * 8, smem_desc_sw128(sv + kk * 2048, BN * 128, 1024), idesc_pv,
                  (acc || kk > 0) ? 1u : 0u);
-        mma_commit(&o_done[t]);
+        mma_commit_warp(&o_done[t]);
       };
 
       wait_slot(0);
       if (active(rg[0], ulo)) qk(0, 0);
       if (active(rg[1], ulo)) qk(1, 0);
-      mma_commit(&kv_empty[0]);
+      mma_commit_warp(&kv_empty[0]);
       for (int j = ulo; j < uhi; ++j) {
         const int itV = 2 * (j - ulo) + 1, itK1 = itV + 1;
         const bool more = j + 1 < uhi;
         wait_slot(itV);
-        TRACE(12, j);
+        if (lane == 0) TRACE(12, j);
         if (active(rg[0], j)) pv(0, itV, j > rg[0].lo);
-        TRACE(0, j);
+        if (lane == 0) TRACE(0, j);
         if (more) {
           wait_slot(itK1);
-          TRACE(15, j);
+          if (lane == 0) TRACE(15, j);
           if (active(rg[0], j + 1)) qk(0, itK1);
         }
-        TRACE(1, j);
+        if (lane == 0) TRACE(1, j);
         if (active(rg[1], j)) pv(1, itV, j > rg[1].lo);
-        TRACE(2, j);
-        mma_commit(&kv_empty[itV % C::kStages]);
+        if (lane == 0) TRACE(2, j);
+        mma_commit_warp(&kv_empty[itV % C::kStages]);
         if (more) {
           if (active(rg[1], j + 1)) qk(1, itK1);
-          mma_commit(&kv_empty[itK1 % C::kStages]);
+          mma_commit_warp(&kv_empty[itK1 % C::kStages]);
         }
       }
     }
