@@ -96,7 +96,8 @@ def tensor(seed: int, tensor_id: int, shape, dtype: str = "bf16", start: int = 0
            count: int | None = None) -> np.ndarray:
     """Generate a full tensor (or a flat slice of it).
 
-    dtype "bf16" returns uint16 bit patterns, "f32" returns float32 values.
+    dtype "bf16" / "f16" return uint16 bit patterns (RNE from the fp32 value),
+    "f32" returns float32 values.
     The slice form lets the oracle regenerate any (b, h) slab of a tensor too
     large to materialise on the host.
     """
@@ -104,6 +105,8 @@ def tensor(seed: int, tensor_id: int, shape, dtype: str = "bf16", start: int = 0
     x = normal_f32(stream_key(seed, tensor_id), start, n)
     if dtype == "bf16":
         x = f32_to_bf16_bits(x)
+    elif dtype == "f16":
+        x = x.astype(np.float16).view(np.uint16)      # IEEE round-to-nearest-even
     elif dtype != "f32":
         raise ValueError(f"unsupported dtype {dtype}")
     return x.reshape(shape) if count is None else x
@@ -113,6 +116,8 @@ def as_f64(x: np.ndarray, dtype: str) -> np.ndarray:
     """Exact fp64 view of generated values (bf16 bits or fp32)."""
     if dtype == "bf16":
         return bf16_bits_to_f32(x).astype(np.float64)
+    if dtype == "f16":
+        return np.asarray(x, dtype=np.uint16).view(np.float16).astype(np.float64)
     return np.asarray(x, dtype=np.float32).astype(np.float64)
 
 

@@ -31,10 +31,10 @@ def _load():
 
 def fill_(t: torch.Tensor, seed: int, tensor_id: int, start: int = 0) -> torch.Tensor:
     """Fill a contiguous CUDA tensor (bf16 or fp32) with elements [start, start + numel)."""
-    if not (t.is_cuda and t.is_contiguous() and t.dtype in (torch.bfloat16, torch.float32)):
-        raise ValueError("need a contiguous bf16/fp32 CUDA tensor")
+    if not (t.is_cuda and t.is_contiguous() and t.dtype in (torch.bfloat16, torch.float16, torch.float32)):
+        raise ValueError("need a contiguous bf16/fp16/fp32 CUDA tensor")
     err = _load().datagen_fill(t.data_ptr(), t.numel(), stream_key(seed, tensor_id), start,
-                               1 if t.dtype == torch.bfloat16 else 0, float(np.float32(INV_SIGMA_F32)),
+                               {torch.bfloat16: 1, torch.float16: 2}.get(t.dtype, 0), float(np.float32(INV_SIGMA_F32)),
                                ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
     if err != 0:
         raise RuntimeError(f"datagen_fill failed with cudaError {err}")
@@ -45,8 +45,9 @@ def tensor(seed: int, tensor_id: int, shape, dtype=torch.bfloat16, device="cuda"
     return fill_(torch.empty(shape, dtype=dtype, device=device), seed, tensor_id)
 
 
-def to_device(x: np.ndarray, device="cuda") -> torch.Tensor:
-    """Upload host generator output (uint16 bf16 bits or fp32) unchanged."""
+def to_device(x: np.ndarray, device="cuda", dtype: str = "bf16") -> torch.Tensor:
+    """Upload host generator output (uint16 bf16/fp16 bits or fp32) unchanged."""
     if x.dtype == np.uint16:
-        return torch.from_numpy(x.view(np.int16).copy()).view(torch.bfloat16).to(device)
+        tdt = torch.float16 if dtype == "f16" else torch.bfloat16
+        return torch.from_numpy(x.view(np.int16).copy()).view(tdt).to(device)
     return torch.from_numpy(np.ascontiguousarray(x)).to(device)

@@ -6,7 +6,8 @@
 //   int datagen_fill(void* dst, long long count, unsigned long long key,
 //                    long long start, int bf16, float inv_sigma, cudaStream_t stream);
 // writes elements [start, start + count) of stream `key` (bf16 bits when
-// bf16 != 0, else fp32).  Returns a cudaError_t value.
+// bf16 == 1, fp16 bits when bf16 == 2, else fp32).  Returns a cudaError_t value.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -29,7 +30,9 @@ __global__ void fill_kernel(void* dst, long long count, uint64_t key, long long 
     const uint64_t base = key + (2ull * idx + 1ull) * G;
     const int64_t s = fields(mix64(base)) + fields(mix64(base + G)) - 4 * 65535;
     const float x = __fmul_rn((float)s, inv_sigma);  // (float)s is exact: |s| < 2^24
-    if (bf16) {
+    if (bf16 == 2) {
+      static_cast<__half*>(dst)[i] = __float2half_rn(x);
+    } else if (bf16) {
       const uint32_t b = __float_as_uint(x);
       const uint32_t r = (b + 0x7FFFu + ((b >> 16) & 1u)) >> 16;
       static_cast<uint16_t*>(dst)[i] = (uint16_t)r;

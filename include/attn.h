@@ -34,7 +34,7 @@
  * - Tensors are caller-owned DEVICE memory, logical layout [B][H][S][D]
  *   ("BHSD", Fig. 8's (B, N, S, H)) described by attn_tensor:
  *   element strides for b, h, s; the D dimension must be contiguous.
- *   bf16 tensors: base 16-byte aligned, strides multiples of 8 elements
+ *   bf16/fp16 tensors: base 16-byte aligned, strides multiples of 8 elements
  *   (TMA requirement) -- else ATTN_ERR_ALIGNMENT.
  * - Calls are asynchronous on `stream`; they never synchronise the host and
  *   never allocate device memory, so they are CUDA-graph capturable.
@@ -75,7 +75,8 @@ typedef enum {
 
 typedef enum {
   ATTN_BF16 = 0, /* bf16 in/out, fp32 accumulation (tcgen05 / decode kernels) */
-  ATTN_FP32 = 1  /* fp32 in/out, fp32 SIMT path (head_dim <= 256) */
+  ATTN_FP32 = 1, /* fp32 in/out, fp32 SIMT path (head_dim <= 256) */
+  ATTN_FP16 = 2  /* fp16 in/out, fp32 accumulation: the paper's precision */
 } attn_dtype;
 
 /* A [B][H][S][D] view. Strides are in ELEMENTS of the tensor's dtype. */
@@ -88,7 +89,7 @@ typedef struct {
 typedef struct {
   int32_t batch, heads_q, heads_kv;   /* heads_q % heads_kv == 0 (GQA group G) */
   int32_t seqlen_q, seqlen_kv;        /* local extents of q and of k/v         */
-  int32_t head_dim;                   /* D: bf16 {64, 128}; fp32 1..256          */
+  int32_t head_dim;                   /* D: bf16/fp16 {64, 128}; fp32 1..256     */
   attn_dtype dtype;
   float scale;                        /* > 0, finite; configs use 1/sqrt(D)      */
   float softcap;                      /* 0 = off; else > 0, finite               */
@@ -129,14 +130,14 @@ typedef struct {
  *   q [B][Hq][Sq][D], k/v [B][Hkv][Skv][D], o [B][Hq][Sq][D] (q's dtype).
  *   lse: nullable DEVICE fp32 [B][Hq][Sq] contiguous.
  * Errors: INVALID_ARGUMENT (extents < 1, heads_q % heads_kv, bad scale /
- * softcap / window, offsets), ALIGNMENT, UNSUPPORTED (bf16 D not in {64,128};
+ * softcap / window, offsets), ALIGNMENT, UNSUPPORTED (bf16/fp16 D not in {64,128};
  * fp32 D > 256), CUDA.
  * ------------------------------------------------------------------- */
 ATTN_API attn_status attn_fused_fwd(const attn_problem* prob, attn_tensor q, attn_tensor k, attn_tensor v,
                            attn_tensor o, float* lse, attn_stream_t stream);
 
 /* ---------------------------------------------------------------------
- * Split-K Update decode (Alg. 2, Fig. 5): seqlen_q must be 1, dtype bf16,
+ * Split-K Update decode (Alg. 2, Fig. 5): seqlen_q must be 1, dtype bf16 or fp16,
  * D in {64, 128}.  The KV axis of every (b, hkv) is cut into num_splits
  * contiguous parts (PrivatizeReduce); each CTA streams its part
  * of K and V once from HBM for all G query heads of the group and emits one

@@ -23,7 +23,7 @@ from ._ffi import AttnParts, AttnProblem, AttnTensor, check, load
 __all__ = ["fused_fwd", "splitkv_decode", "combine", "default_splits", "workspace_bytes",
            "last_launch_count", "Parts", "load"]
 
-_DT = {torch.bfloat16: _ffi.ATTN_BF16, torch.float32: _ffi.ATTN_FP32}
+_DT = {torch.bfloat16: _ffi.ATTN_BF16, torch.float32: _ffi.ATTN_FP32, torch.float16: _ffi.ATTN_FP16}
 
 
 def _as_tensor(t: Optional[torch.Tensor]) -> AttnTensor:

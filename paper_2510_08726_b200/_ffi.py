@@ -17,6 +17,7 @@ ATTN_ERR_WORKSPACE_TOO_SMALL = 4
 ATTN_ERR_CUDA = 5
 ATTN_BF16 = 0
 ATTN_FP32 = 1
+ATTN_FP16 = 2
 ATTN_Q_POS_DEFAULT = -(1 << 63)
 
 EXPORTED = ("attn_fused_fwd", "attn_splitkv_default_splits", "attn_splitkv_workspace_bytes",

@@ -53,14 +53,14 @@ EncodeFn get_encode() {
 
 // 4-D bf16 map over [B][H][S][D] (dims listed innermost first), box (box_d, box_s, 1, 1).
 attn_status make_map(CUtensorMap* m, const attn_tensor& t, int B, int H, int S, int D, int box_d, int box_s,
-                     bool swizzle128) {
+                     bool swizzle128, bool f16 = false) {
   EncodeFn enc = get_encode();
   if (!enc) return fail(ATTN_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
   cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)S, (cuuint64_t)H, (cuuint64_t)B};
   cuuint64_t strides[3] = {(cuuint64_t)t.stride_s * 2, (cuuint64_t)t.stride_h * 2, (cuuint64_t)t.stride_b * 2};
   cuuint32_t box[4] = {(cuuint32_t)box_d, (cuuint32_t)box_s, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, t.ptr, dims, strides, box, estr,
+  CUresult r = enc(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, t.ptr, dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE,
                    swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -94,7 +94,7 @@ attn_status check_problem(const attn_problem* p, attn::VariantParams* vp) {
   CHECK_ARG(isfinite(p->softcap) && p->softcap >= 0.f, "softcap must be finite and >= 0");
   CHECK_ARG(p->window_left >= -1 && p->window_right >= -1, "window bounds must be >= -1");
   CHECK_ARG(p->causal == 0 || p->causal == 1, "causal must be 0 or 1");
-  CHECK_ARG(p->dtype == ATTN_BF16 || p->dtype == ATTN_FP32, "unknown dtype");
+  CHECK_ARG(p->dtype == ATTN_BF16 || p->dtype == ATTN_FP32 || p->dtype == ATTN_FP16, "unknown dtype");
   const int64_t total = p->seqlen_kv_total == 0 ? p->seqlen_kv : p->seqlen_kv_total;
   CHECK_ARG(p->kv_pos_offset >= 0 && p->kv_pos_offset + p->seqlen_kv <= total,
             "need 0 <= kv_pos_offset and kv_pos_offset + seqlen_kv <= seqlen_kv_total");
@@ -163,24 +163,25 @@ attn_status attn_fused_fwd(const attn_problem* prob, attn_tensor q, attn_tensor 
   attn_status st = check_problem(prob, &vp);
   if (st != ATTN_OK) return st;
   const attn_problem& p = *prob;
-  const int eb = p.dtype == ATTN_BF16 ? 2 : 4;
+  const int eb = p.dtype == ATTN_FP32 ? 4 : 2;
   if ((st = check_tensor(q, "q", eb, p.batch, p.heads_q, p.seqlen_q)) != ATTN_OK) return st;
   if ((st = check_tensor(k, "k", eb, p.batch, p.heads_kv, p.seqlen_kv)) != ATTN_OK) return st;
   if ((st = check_tensor(v, "v", eb, p.batch, p.heads_kv, p.seqlen_kv)) != ATTN_OK) return st;
   if ((st = check_tensor(o, "o", eb, p.batch, p.heads_q, p.seqlen_q)) != ATTN_OK) return st;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   int launches = 0;
-  if (p.dtype == ATTN_BF16) {
+  if (p.dtype == ATTN_BF16 || p.dtype == ATTN_FP16) {
     if (p.head_dim != 64 && p.head_dim != 128)
-      return fail(ATTN_ERR_UNSUPPORTED, "bf16 head_dim must be 64 or 128 (got %d)", p.head_dim);
+      return fail(ATTN_ERR_UNSUPPORTED, "bf16/fp16 head_dim must be 64 or 128 (got %d)", p.head_dim);
     attn::FwdTcArgs a;
     a.s = shape_of(prob);
+    a.f16 = p.dtype == ATTN_FP16;
     a.v = vp;
     a.lse = lse;
-    if ((st = make_map(&a.tm_q, q, p.batch, p.heads_q, p.seqlen_q, p.head_dim, 64, 128, true)) != ATTN_OK) return st;
-    if ((st = make_map(&a.tm_k, k, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, 128, true)) != ATTN_OK) return st;
-    if ((st = make_map(&a.tm_v, v, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, 128, true)) != ATTN_OK) return st;
-    if ((st = make_map(&a.tm_o, o, p.batch, p.heads_q, p.seqlen_q, p.head_dim, 64, 128, true)) != ATTN_OK) return st;
+    if ((st = make_map(&a.tm_q, q, p.batch, p.heads_q, p.seqlen_q, p.head_dim, 64, 128, true, a.f16)) != ATTN_OK) return st;
+    if ((st = make_map(&a.tm_k, k, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, 128, true, a.f16)) != ATTN_OK) return st;
+    if ((st = make_map(&a.tm_v, v, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, 128, true, a.f16)) != ATTN_OK) return st;
+    if ((st = make_map(&a.tm_o, o, p.batch, p.heads_q, p.seqlen_q, p.head_dim, 64, 128, true, a.f16)) != ATTN_OK) return st;
     st = cuda_status(attn::launch_fwd_tc(a, s, &launches), "fwd_tc launch");
   } else {
     if (p.head_dim > 256) return fail(ATTN_ERR_UNSUPPORTED, "fp32 head_dim must be <= 256");
@@ -232,7 +233,7 @@ attn_status attn_splitkv_decode(const attn_problem* prob, attn_tensor q, attn_te
   if (st != ATTN_OK) return st;
   const attn_problem& p = *prob;
   if (p.seqlen_q != 1) return fail(ATTN_ERR_UNSUPPORTED, "decode requires seqlen_q == 1 (got %d)", p.seqlen_q);
-  if (p.dtype != ATTN_BF16) return fail(ATTN_ERR_UNSUPPORTED, "decode supports bf16 only");
+  if (p.dtype == ATTN_FP32) return fail(ATTN_ERR_UNSUPPORTED, "decode supports bf16 and fp16 only");
   if (p.head_dim != 64 && p.head_dim != 128)
     return fail(ATTN_ERR_UNSUPPORTED, "decode head_dim must be 64 or 128 (got %d)", p.head_dim);
   const int G = p.heads_q / p.heads_kv;
@@ -247,6 +248,7 @@ attn_status attn_splitkv_decode(const attn_problem* prob, attn_tensor q, attn_te
 
   attn::DecodeArgs a;
   a.s = shape_of(prob);
+  a.f16 = p.dtype == ATTN_FP16;
   a.v = vp;
   a.q = static_cast<const uint16_t*>(q.ptr);
   a.q_sb = q.stride_b;
@@ -276,8 +278,8 @@ attn_status attn_splitkv_decode(const attn_problem* prob, attn_tensor q, attn_te
     a.parts = attn::PartsView{m, l, ob, num_splits, bh, p.heads_q, 1, bh * p.head_dim,
                               (long long)p.heads_q * p.head_dim, p.head_dim};
   }
-  if ((st = make_map(&a.tm_k, k, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, nk, true)) != ATTN_OK) return st;
-  if ((st = make_map(&a.tm_v, v, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, nk, true)) != ATTN_OK) return st;
+  if ((st = make_map(&a.tm_k, k, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, nk, true, a.f16)) != ATTN_OK) return st;
+  if ((st = make_map(&a.tm_v, v, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, nk, true, a.f16)) != ATTN_OK) return st;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   int launches = 0;
   st = cuda_status(attn::launch_decode(a, s, &launches), "decode launch");
@@ -288,7 +290,7 @@ attn_status attn_splitkv_decode(const attn_problem* prob, attn_tensor q, attn_te
     c.H = p.heads_q;
     c.D = p.head_dim;
     c.in = a.parts;
-    c.out_bf16 = 1;
+    c.out_bf16 = a.f16 ? 2 : 1;
     c.o = o.ptr;
     c.o_sb = o.stride_b;
     c.o_sh = o.stride_h;
@@ -308,7 +310,7 @@ attn_status attn_combine(int32_t batch, int32_t heads, int32_t head_dim, const a
   if (head_dim > 256) return fail(ATTN_ERR_UNSUPPORTED, "combine head_dim must be <= 256");
   CHECK_ARG(in != nullptr && in->m && in->l && in->o && in->num_parts >= 1, "bad input parts");
   CHECK_ARG(o.ptr != nullptr || lse != nullptr || acc_out != nullptr, "no output requested");
-  CHECK_ARG(out_dtype == ATTN_BF16 || out_dtype == ATTN_FP32, "unknown out dtype");
+  CHECK_ARG(out_dtype == ATTN_BF16 || out_dtype == ATTN_FP32 || out_dtype == ATTN_FP16, "unknown out dtype");
   if (acc_out) CHECK_ARG(acc_out->m && acc_out->l && acc_out->o && acc_out->num_parts == 1, "bad acc_out");
   attn::CombineArgs c{};
   c.B = batch;
@@ -316,7 +318,7 @@ attn_status attn_combine(int32_t batch, int32_t heads, int32_t head_dim, const a
   c.D = head_dim;
   c.in = attn::PartsView{in->m, in->l, in->o, in->num_parts, in->m_stride_part, in->m_stride_b, in->m_stride_h,
                          in->o_stride_part, in->o_stride_b, in->o_stride_h};
-  c.out_bf16 = out_dtype == ATTN_BF16;
+  c.out_bf16 = out_dtype == ATTN_BF16 ? 1 : (out_dtype == ATTN_FP16 ? 2 : 0);
   c.o = o.ptr;
   c.o_sb = o.stride_b;
   c.o_sh = o.stride_h;

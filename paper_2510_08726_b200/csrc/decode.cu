@@ -20,6 +20,7 @@
 // exp(m_s - M), L = sum w_s l_s, O = sum w_s O_s; output O / L and
 // lse = M + ln L, or the un-normalised merged triple for hierarchical merges.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <math.h>
 
 #include "kernels.h"
@@ -54,12 +55,20 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t&
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
                : "r"(addr));
 }
+template <bool kF16>
 __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
-      "{%0, %1, %2, %3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+  if constexpr (kF16)
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+        "{%0, %1, %2, %3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+  else
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+        "{%0, %1, %2, %3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
 // Byte offset of 16-byte chunk `ch` (0 .. D/8-1) of row `key` in a stage tile
@@ -68,7 +77,7 @@ __device__ __forceinline__ uint32_t tile_off(int key, int ch) {
   return (ch >> 3) * (NK * 128) + key * 128 + (((ch & 7) ^ (key & 7)) << 4);
 }
 
-template <int D, bool kAlibi, bool kSoftcap>
+template <int D, bool kAlibi, bool kSoftcap, bool kF16>
 __global__ void __launch_bounds__(kThreads) decode_split_kernel(const __grid_constant__ CUtensorMap tm_k,
                                                                 const __grid_constant__ CUtensorMap tm_v,
                                                                 const DecodeArgs a) {
@@ -163,8 +172,8 @@ __global__ void __launch_bounds__(kThreads) decode_split_kernel(const __grid_con
       for (int kk = 0; kk < D / 16; ++kk) {
         uint32_t b0, b1, b2, b3;
         ldsm_x4(sk + tile_off(key, kk * 2 + sub), b0, b1, b2, b3);
-        mma16816(s[0], qa[kk], b0, b1);
-        mma16816(s[1], qa[kk], b2, b3);
+        mma16816<kF16>(s[0], qa[kk], b0, b1);
+        mma16816<kF16>(s[1], qa[kk], b2, b3);
       }
     }
     // score_mod + mask (log2 units); this thread holds keys kb + n*8 + quad*2 + e of row `row`
@@ -203,9 +212,9 @@ __global__ void __launch_bounds__(kThreads) decode_split_kernel(const __grid_con
     }
     // P as the A operand (rows 8..15 zero)
     uint32_t pa[4];
-    pa[0] = pack_bf16x2(p[0], p[1]);
+    pa[0] = pack2<kF16>(p[0], p[1]);
     pa[1] = 0u;
-    pa[2] = pack_bf16x2(p[2], p[3]);
+    pa[2] = pack2<kF16>(p[2], p[3]);
     pa[3] = 0u;
     // O (16 x D) += P V
     {
@@ -215,8 +224,8 @@ __global__ void __launch_bounds__(kThreads) decode_split_kernel(const __grid_con
       for (int nd = 0; nd < D / 8; nd += 2) {
         uint32_t b0, b1, b2, b3;
         ldsm_x4_t(sv + tile_off(key, nd + sub), b0, b1, b2, b3);
-        mma16816(o[nd], pa, b0, b1);
-        mma16816(o[nd + 1], pa, b2, b3);
+        mma16816<kF16>(o[nd], pa, b0, b1);
+        mma16816<kF16>(o[nd + 1], pa, b2, b3);
       }
     }
     __syncwarp();
@@ -306,8 +315,10 @@ __global__ void __launch_bounds__(128) combine_kernel(const CombineArgs a) {
       const int d = lane + 32 * r;
       if (d >= a.D) continue;
       const long long oi = (long long)b * a.o_sb + (long long)h * a.o_sh + d;
-      if (a.out_bf16)
+      if (a.out_bf16 == 1)
         reinterpret_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(acc[r] * inv);
+      else if (a.out_bf16 == 2)
+        reinterpret_cast<__half*>(a.o)[oi] = __float2half_rn(acc[r] * inv);
       else
         reinterpret_cast<float*>(a.o)[oi] = acc[r] * inv;
     }
@@ -328,10 +339,10 @@ __global__ void __launch_bounds__(128) combine_kernel(const CombineArgs a) {
   }
 }
 
-template <int D, bool kAlibi, bool kSoftcap>
+template <int D, bool kAlibi, bool kSoftcap, bool kF16>
 cudaError_t launch_dec_t(const DecodeArgs& a, cudaStream_t stream) {
   using C = DCfg<D>;
-  auto kern = decode_split_kernel<D, kAlibi, kSoftcap>;
+  auto kern = decode_split_kernel<D, kAlibi, kSoftcap, kF16>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
   if (e != cudaSuccess) return e;
   dim3 grid(a.num_splits, a.s.Hkv, a.s.B);
@@ -339,13 +350,13 @@ cudaError_t launch_dec_t(const DecodeArgs& a, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
-template <int D>
+template <int D, bool kF16>
 cudaError_t launch_dec_d(const DecodeArgs& a, cudaStream_t stream) {
   const bool alibi = a.v.alibi != nullptr, cap = a.v.softcap > 0.f;
-  if (alibi && cap) return launch_dec_t<D, true, true>(a, stream);
-  if (alibi) return launch_dec_t<D, true, false>(a, stream);
-  if (cap) return launch_dec_t<D, false, true>(a, stream);
-  return launch_dec_t<D, false, false>(a, stream);
+  if (alibi && cap) return launch_dec_t<D, true, true, kF16>(a, stream);
+  if (alibi) return launch_dec_t<D, true, false, kF16>(a, stream);
+  if (cap) return launch_dec_t<D, false, true, kF16>(a, stream);
+  return launch_dec_t<D, false, false, kF16>(a, stream);
 }
 
 }  // namespace
@@ -353,7 +364,8 @@ cudaError_t launch_dec_d(const DecodeArgs& a, cudaStream_t stream) {
 int decode_stage_keys(int, int) { return NK; }
 
 cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t stream, int* launches) {
-  cudaError_t e = a.s.D == 128 ? launch_dec_d<128>(a, stream) : launch_dec_d<64>(a, stream);
+  cudaError_t e = a.f16 ? (a.s.D == 128 ? launch_dec_d<128, true>(a, stream) : launch_dec_d<64, true>(a, stream))
+                        : (a.s.D == 128 ? launch_dec_d<128, false>(a, stream) : launch_dec_d<64, false>(a, stream));
   if (e == cudaSuccess && launches) ++*launches;
   return e;
 }

@@ -185,7 +185,7 @@ __device__ __forceinline__ float score_tile(float (&x)[BN], const VariantParams&
   return mt;
 }
 
-template <int D, bool kAlibi, bool kSoftcap>
+template <int D, bool kAlibi, bool kSoftcap, bool kF16>
 __global__ void __launch_bounds__(kThreads, 1)
     fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o, const Shape s,
@@ -295,8 +295,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // The whole warp runs this role with warp-uniform values; one elected lane
     // issues each tcgen05 instruction (see mma_*_warp).
     if (uhi > ulo) {
-      constexpr uint32_t idesc_qk = idesc_bf16_f32(BM, BN, 0, 0);  // Q K-major, K K-major
-      constexpr uint32_t idesc_pv = idesc_bf16_f32(BM, D, 0, 1);   // P (TMEM), V MN-major
+      constexpr uint32_t idesc_qk = idesc_f16_f32(BM, BN, 0, 0, !kF16);  // Q K-major, K K-major
+      constexpr uint32_t idesc_pv = idesc_f16_f32(BM, D, 0, 1, !kF16);   // P (TMEM), V MN-major
       const uint32_t tS[2] = {tmem, tmem + 128};
       const uint32_t tO[2] = {tmem + 256, tmem + 384};
       const Range rg[2] = {rng0, rng1};
@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           sum0 += p0;
           sum1 += p1;
-          pk[e] = pack_bf16x2(p0, p1);
+          pk[e] = pack2<kF16>(p0, p1);
         }
         tmem_st16(tS + c0 / 2, pk);
       }
@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         uint32_t pk[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) pk[e] = pack_bf16x2(u2f(o[2 * e]) * inv_l, u2f(o[2 * e + 1]) * inv_l);
+        for (int e = 0; e < 16; ++e) pk[e] = pack2<kF16>(u2f(o[2 * e]) * inv_l, u2f(o[2 * e + 1]) * inv_l);
         uint8_t* rowp = sOut + (c >> 1) * (BM * 128) + r * 128;
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
@@ -540,10 +540,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int D, bool kAlibi, bool kSoftcap>
+template <int D, bool kAlibi, bool kSoftcap, bool kF16>
 cudaError_t launch_t(const FwdTcArgs& a, cudaStream_t stream) {
   using C = Cfg<D>;
-  auto kern = fwd_tc_kernel<D, kAlibi, kSoftcap>;
+  auto kern = fwd_tc_kernel<D, kAlibi, kSoftcap, kF16>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
   if (e != cudaSuccess) return e;
   dim3 grid((a.s.Sq + 2 * BM - 1) / (2 * BM), a.s.Hq, a.s.B);
@@ -551,13 +551,13 @@ cudaError_t launch_t(const FwdTcArgs& a, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
-template <int D>
+template <int D, bool kF16>
 cudaError_t launch_d(const FwdTcArgs& a, cudaStream_t stream) {
   const bool alibi = a.v.alibi != nullptr, cap = a.v.softcap > 0.f;
-  if (alibi && cap) return launch_t<D, true, true>(a, stream);
-  if (alibi) return launch_t<D, true, false>(a, stream);
-  if (cap) return launch_t<D, false, true>(a, stream);
-  return launch_t<D, false, false>(a, stream);
+  if (alibi && cap) return launch_t<D, true, true, kF16>(a, stream);
+  if (alibi) return launch_t<D, true, false, kF16>(a, stream);
+  if (cap) return launch_t<D, false, true, kF16>(a, stream);
+  return launch_t<D, false, false, kF16>(a, stream);
 }
 
 }  // namespace
@@ -569,7 +569,8 @@ extern "C" __attribute__((visibility("default"))) int attn_debug_trace(long long
 #endif
 
 cudaError_t launch_fwd_tc(const FwdTcArgs& a, cudaStream_t stream, int* launches) {
-  cudaError_t e = a.s.D == 128 ? launch_d<128>(a, stream) : launch_d<64>(a, stream);
+  cudaError_t e = a.f16 ? (a.s.D == 128 ? launch_d<128, true>(a, stream) : launch_d<64, true>(a, stream))
+                        : (a.s.D == 128 ? launch_d<128, false>(a, stream) : launch_d<64, false>(a, stream));
   if (e == cudaSuccess && launches) ++*launches;
   return e;
 }

@@ -29,6 +29,7 @@ struct Shape {
 // ------------------------------------------------------------ tcgen05 prefill
 struct FwdTcArgs {
   Shape s;
+  bool f16;    // fp16 inputs/outputs (else bf16)
   VariantParams v;
   float* lse;  // nullable, [B][Hq][Sq]
   CUtensorMap tm_q, tm_k, tm_v, tm_o;
@@ -53,8 +54,9 @@ struct PartsView {
 };
 struct DecodeArgs {
   Shape s;
+  bool f16;                     // fp16 inputs (else bf16)
   VariantParams v;
-  const uint16_t* q;            // bf16 bits
+  const uint16_t* q;            // bf16 / fp16 bits
   long long q_sb, q_sh;
   int num_splits, split_len;    // keys per split (multiple of the stage size)
   PartsView parts;              // destination of the local-section triples
@@ -67,7 +69,7 @@ int decode_stage_keys(int G, int D);
 struct CombineArgs {
   int B, H, D;
   PartsView in;
-  int out_bf16;                 // 1: bf16 out, 0: fp32 out
+  int out_bf16;                 // 1: bf16 out, 2: fp16 out, 0: fp32 out
   void* o; long long o_sb, o_sh;  // nullable
   float* lse;                   // nullable [B][H]
   PartsView acc;                // acc.m == nullptr => not written

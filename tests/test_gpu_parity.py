@@ -61,7 +61,7 @@ FP32_CASES = [
 
 
 @pytest.mark.parametrize("case", range(len(FP32_CASES)))
-def test_fp32_forward(case):
+def test_fp32_forward(case):  # noqa: D103
     c = dict(FP32_CASES[case])
     B, Hq, Hkv, S, D = c.pop("B"), c.pop("Hq"), c.pop("Hkv"), c.pop("S"), c.pop("D")
     kw = {}
@@ -304,3 +304,42 @@ def test_host_buffers_end_to_end():
     o = pb.fused_fwd(*host, causal=True)
     assert o.device.type == "cpu"
     assert_bf16_close(o.float().numpy().astype(np.float64), ref_o, "host e2e")
+
+
+# --------------------------------------------------------------------------- fp16 inputs (NEXT-1, the paper's precision P:946)
+def test_device_generator_fp16_is_bit_identical():
+    host = datagen.tensor(999, 3, (2, 3, 50, 64), "f16")
+    dev = dgd.tensor(999, 3, (2, 3, 50, 64), torch.float16).cpu()
+    np.testing.assert_array_equal(dev.view(torch.int16).numpy().view(np.uint16), host)
+
+
+@pytest.mark.parametrize("D", [128, 64])
+@pytest.mark.parametrize("name", ["global", "causal", "alibi_causal", "softcap_causal", "window_band"])
+def test_fp16_prefill_small(name, D):
+    kw = dict(VARIANTS[name])
+    B, Hq, Hkv, S = 1, 4, 2, 300
+    if kw.pop("alibi", False):
+        kw["alibi_slopes"] = datagen.alibi_slopes(Hq)
+    p = problem(B, Hq, Hkv, S, S, D, **kw)
+    raw, f64 = gen_qkv(4000 + D, B, Hq, Hkv, S, S, D, "f16")
+    ref_o, ref_l = oracle.attention(p, *f64)
+    q, k, v = (dgd.to_device(x, dtype="f16") for x in raw)
+    o, lse = pb.fused_fwd(q, k, v, return_lse=True, **_kw_from(p))
+    assert o.dtype == torch.float16
+    assert_bf16_close(o.float().cpu().numpy().astype(np.float64), ref_o, f"fp16 {name} D={D}")
+    assert_lse_close(lse.cpu().numpy(), ref_l, LSE_TOL_BF16, "fp16 lse")
+
+
+@pytest.mark.parametrize("case", [0, 2, 6])
+def test_fp16_decode(case):
+    c = dict(DECODE_CASES[case])
+    B, Hq, Hkv, Skv, D, splits = (c.pop(k) for k in ("B", "Hq", "Hkv", "Skv", "D", "splits"))
+    if c.pop("alibi", False):
+        c["alibi_slopes"] = datagen.alibi_slopes(Hq)
+    p = problem(B, Hq, Hkv, 1, Skv, D, **c)
+    raw, f64 = gen_qkv(5000 + case, B, Hq, Hkv, 1, Skv, D, "f16")
+    ref_o, _ = oracle.attention(p, *f64)
+    q, k, v = (dgd.to_device(x, dtype="f16") for x in raw)
+    o = pb.splitkv_decode(q, k, v, num_splits=splits, **_kw_from(p))
+    assert o.dtype == torch.float16
+    assert_bf16_close(o.float().cpu().numpy().astype(np.float64), ref_o, f"fp16 decode {case}")
