@@ -274,11 +274,13 @@ def main_gpu(args):
     flops = 4.0 * D * allowed_pairs(S, var) * B * Hq
     value = world * flops / (ms * 1e-3) / 1e12
     achieved = flops / (ms * 1e-3) / 1e12
-    traffic = None
+    traffic, traffic_decode = None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(f"fwd_{name}")
+            tr = json.load(open(tpath))
+            traffic = tr.get(f"fwd_{name}")
+            traffic_decode = tr.get(f"decode_b{args.decode_batch}") if world == 1 else None
         except Exception:
             traffic = None
     line = {
@@ -313,32 +315,44 @@ def main_gpu(args):
 
     # ------------------------------------------------------------- decode (secondary metric)
     if not args.no_decode:
-        Bd, Hqd, Hkvd, L, Dd = args.decode_batch, 32, 8, 131072, 128
+        Hqd, Hkvd, L, Dd = 32, 8, 131072, 128
         seed5 = datagen.config_seed(5)
         lo, hi = pdist.shard_range(L, rank, world)
-        qd = torch.empty(Bd, Hqd, 1, Dd, dtype=torch.bfloat16, device=dev)
-        dgd.fill_(qd, seed5, 1)
-        kd = torch.empty(Bd, Hkvd, hi - lo, Dd, dtype=torch.bfloat16, device=dev)
-        vd = torch.empty_like(kd)
-        for b in range(Bd):
-            for h in range(Hkvd):
-                start = ((b * Hkvd + h) * L + lo) * Dd
-                dgd.fill_(kd[b, h], seed5, 2, start=start)
-                dgd.fill_(vd[b, h], seed5, 3, start=start)
-        od = torch.empty_like(qd)
-        ws = torch.empty(pb.workspace_bytes(qd, kd), dtype=torch.uint8, device=dev)
-        if world == 1:
-            dstep = lambda: pb.splitkv_decode(qd, kd, vd, causal=True, out=od, workspace=ws)  # noqa: E731
-        else:
-            dstep = lambda: pdist.decode_kv_sharded(qd, kd, vd, kv_pos_offset=lo, seqlen_kv_total=L,  # noqa: E731
-                                                    causal=True)
-        dstep()
-        torch.cuda.synchronize()
-        dl = pb.last_launch_count()
-        dms, dclk = timed(dstep, args.steps, args.warmup)
-        kv_bytes = 2.0 * Bd * Hkvd * L * Dd * 2
-        gbs = kv_bytes / (dms * 1e-3) / 1e9
-        per_rank = kv_bytes / world / (dms * 1e-3) / 1e9
+
+        def run_decode(Bd, steps, warmup):
+            qd = torch.empty(Bd, Hqd, 1, Dd, dtype=torch.bfloat16, device=dev)
+            dgd.fill_(qd, seed5, 1)
+            kd = torch.empty(Bd, Hkvd, hi - lo, Dd, dtype=torch.bfloat16, device=dev)
+            vd = torch.empty_like(kd)
+            for b in range(Bd):
+                for h in range(Hkvd):
+                    start = ((b * Hkvd + h) * L + lo) * Dd
+                    dgd.fill_(kd[b, h], seed5, 2, start=start)
+                    dgd.fill_(vd[b, h], seed5, 3, start=start)
+            od = torch.empty_like(qd)
+            ws = torch.empty(pb.workspace_bytes(qd, kd), dtype=torch.uint8, device=dev)
+            if world == 1:
+                dstep = lambda: pb.splitkv_decode(qd, kd, vd, causal=True, out=od, workspace=ws)  # noqa: E731
+            else:
+                dstep = lambda: pdist.decode_kv_sharded(qd, kd, vd, kv_pos_offset=lo,  # noqa: E731
+                                                        seqlen_kv_total=L, causal=True)
+            dstep()
+            torch.cuda.synchronize()
+            nl = pb.last_launch_count()
+            dms, dclk = timed(dstep, steps, warmup)
+            del qd, kd, vd, od, ws
+            torch.cuda.empty_cache()
+            kv_bytes = 2.0 * Bd * Hkvd * L * Dd * 2
+            return kv_bytes, dms, dclk, nl
+
+        sweep = {}
+        for Bd in sorted(set([1, 4, args.decode_batch])):
+            kv_bytes, dms, dclk, dl = run_decode(Bd, max(args.steps, 20), args.warmup)
+            sweep[Bd] = {"GB/s": kv_bytes / (dms * 1e-3) / 1e9, "ms_per_step": dms,
+                         "frac_of_hbm_peak": kv_bytes / world / (dms * 1e-3) / 1e9 / peaks["hbm"]}
+        Bd = args.decode_batch
+        gbs, dms = sweep[Bd]["GB/s"], sweep[Bd]["ms_per_step"]
+        per_rank = gbs / world
         line["decode"] = {
             "metric": "split-KV decode HBM GB/s (K+V bytes read once / time)", "value": gbs, "unit": "GB/s",
             "ms_per_step": dms, "scaling": "strong" if world > 1 else None, "clocks": dclk,
@@ -346,12 +360,13 @@ def main_gpu(args):
                        "kv_len": L, "head_dim": Dd, "causal": True,
                        "parallelism": f"KV-sequence shard x{world} + NCCL all-gather of (m,l,O)" if world > 1
                        else "single GPU split-KV", "l2": "KV larger than L2"},
+            "batch_sweep": {str(b): {k: round(v, 4) for k, v in d.items()} for b, d in sweep.items()},
             "gpu_launches_per_step": dl,
             "roofline": {"bound": "hbm", "achieved": per_rank, "peak": peaks["hbm"], "unit": "GB/s",
-                         "frac": per_rank / peaks["hbm"], "traffic": None,
-                         "peak_src": f"{peaks['src']} hbm_gbs (copy)", "kernel": "decode_split_kernel + combine"},
+                         "frac": per_rank / peaks["hbm"], "traffic": traffic_decode,
+                         "peak_src": f"{peaks['src']} hbm_gbs (copy)", "kernel": "decode_split_kernel + combine",
+                         "algorithmic_bytes_per_launch": 2.0 * Bd * Hkvd * L * Dd * 2 / world},
         }
-        del qd, kd, vd, od, ws
 
     # ------------------------------------------------------------- CPU baseline (oracle), rank 0, N = 1
     if rank == 0 and world == 1 and not args.no_cpu:

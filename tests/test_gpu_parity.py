@@ -61,7 +61,7 @@ FP32_CASES = [
 
 
 @pytest.mark.parametrize("case", range(len(FP32_CASES)))
-def test_fp32_forward(case):  # noqa: D103
+def test_fp32_forward(case):
     c = dict(FP32_CASES[case])
     B, Hq, Hkv, S, D = c.pop("B"), c.pop("Hq"), c.pop("Hkv"), c.pop("S"), c.pop("D")
     kw = {}
