@@ -46,11 +46,17 @@ constexpr float kTau = 8.0f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr uint32_t kBarTok0 = 3, kBarTok1 = 4;   // named barriers of the exp token
+constexpr uint32_t kBarP0 = 5;                    // 5 / 6: "P_t ready" (128 softmax threads + MMA warp)
 #ifndef ATTN_TOKEN
 #define ATTN_TOKEN 1
 #endif
 constexpr bool kToken = ATTN_TOKEN != 0;   // alternate the two softmax warpgroups' exp phases
 
+#ifdef ATTN_SOFTMAX_SPIN
+#define WAIT_SM(bar, par) mbar_wait_spin(bar, par)   // softmax waits for S: poll
+#else
+#define WAIT_SM(bar, par) mbar_wait(bar, par)        // softmax waits for S: try_wait (HW sleep)
+#endif
 #ifndef ATTN_SLEEP_WAIT
 #define WAIT_LM(bar, par) mbar_wait_spin(bar, par)   // loader / MMA thread waits: poll
 #else
@@ -82,6 +88,9 @@ struct Cfg {
 #else
   static constexpr int kStages = (D == 128) ? 5 : 10;
 #endif
+  // Load-group barriers (ring).  The producer can be at most kStages/2 groups
+  // ahead of the issuer's wait, so kStages/2 + 1 barriers never alias a phase.
+  static constexpr int kPairBars = kStages / 2 + 1;
   static constexpr int kSmemQ = 2 * kQTileBytes;
   static constexpr int kSmemKV = kStages * kKVTileBytes;
   static constexpr int kNumBars = 1 + 2 * kStages + 6;
@@ -239,7 +248,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&s_full[t], 1);
-      mbar_init(&p_ready[t], 4);
       mbar_init(&o_done[t], 1);
     }
     fence_mbarrier_init();
@@ -271,22 +279,29 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_prefetch_4d(&tm_k, bx * 64, j * BN, hkv, b);
           tma_prefetch_4d(&tm_v, bx * 64, j * BN, hkv, b);
         }
-      int it = 0;
-      for (int j = ulo; j < uhi; ++j) {
+      // Load groups: g = 0 is K_ulo; g >= 1 is the pair (V_{ulo+g-1}, K_{ulo+g}) (the last
+      // group has no K).  A group signals ONE "pair" barrier (kv_full[g % C::kPairBars]), so
+      // the MMA issuer waits once per KV step for both tiles it needs next.
+      const int n = uhi - ulo;
+      for (int g = 0; g <= n; ++g) {
+        const int j = ulo + g;
         if (kPrefetch > 0 && j + kPrefetch < uhi)
           for (int bx = 0; bx < C::kBoxes; ++bx) {
             tma_prefetch_4d(&tm_k, bx * 64, (j + kPrefetch) * BN, hkv, b);
             tma_prefetch_4d(&tm_v, bx * 64, (j + kPrefetch) * BN, hkv, b);
           }
-        for (int kind = 0; kind < 2; ++kind, ++it) {
-          const int slot = it % C::kStages;
-          WAIT_LM(&kv_empty[slot], ((it / C::kStages) & 1) ^ 1);
-          TRACE(24 + kind, j);
-          mbar_arrive_expect_tx(&kv_full[slot], C::kKVTileBytes);
-          uint8_t* dst = sKV + slot * C::kKVTileBytes;
-          const CUtensorMap* tm = kind == 0 ? &tm_k : &tm_v;
+        const int it0 = g == 0 ? 0 : 2 * g - 1;          // ring index of the group's first tile
+        const int it1 = g < n ? 2 * g : 2 * g - 1;       // ... and of its last tile
+        for (int it = it0; it <= it1; ++it) WAIT_LM(&kv_empty[it % C::kStages], ((it / C::kStages) & 1) ^ 1);
+        uint64_t* bar = &kv_full[g % C::kPairBars];
+        mbar_arrive_expect_tx(bar, (it1 - it0 + 1) * C::kKVTileBytes);
+        for (int it = it0; it <= it1; ++it) {
+          const bool is_k = (it % 2) == 0;              // even ring index: K_{ulo + it/2}; odd: V_{ulo + it/2}
+          const int jj = ulo + it / 2;
+          TRACE(24 + (is_k ? 0 : 1), jj);
+          uint8_t* dst = sKV + (it % C::kStages) * C::kKVTileBytes;
           for (int bx = 0; bx < C::kBoxes; ++bx)
-            tma_load_4d(tm, &kv_full[slot], dst + bx * BN * 128, bx * 64, j * BN, hkv, b, pol_kv);
+            tma_load_4d(is_k ? &tm_k : &tm_v, bar, dst + bx * BN * 128, bx * 64, jj * BN, hkv, b, pol_kv);
         }
       }
     }
@@ -300,11 +315,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t tS[2] = {tmem, tmem + 128};
       const uint32_t tO[2] = {tmem + 256, tmem + 384};
       const Range rg[2] = {rng0, rng1};
-      uint32_t p_phase[2] = {0, 0};
       WAIT_LM(q_full, 0);
 
-      auto wait_slot = [&](int it) {
-        WAIT_LM(&kv_full[it % C::kStages], (it / C::kStages) & 1);
+      auto wait_group = [&](int g) {   // load group g (see the producer)
+        WAIT_LM(&kv_full[g % C::kPairBars], (g / C::kPairBars) & 1);
         tc_fence_after();
       };
       auto qk = [&](int t, int it) {   // S_t = Q_t K^T
@@ -320,8 +334,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit_warp(&s_full[t]);
       };
       auto pv = [&](int t, int it, bool acc) {   // O_t += P_t V (P straight from TMEM)
-        WAIT_LM(&p_ready[t], p_phase[t]);
-        p_phase[t] ^= 1;
+        named_bar_sync(kBarP0 + t, 160);          // the 128 softmax threads of tile t arrived
         tc_fence_after();
         if (lane == 0) TRACE(13 + t, it / 2);
         const uint32_t sv = smem_u32(sKV + (it % C::kStages) * C::kKVTileBytes);
@@ -332,22 +345,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit_warp(&o_done[t]);
       };
 
-      wait_slot(0);
+      wait_group(0);
       if (active(rg[0], ulo)) qk(0, 0);
       if (active(rg[1], ulo)) qk(1, 0);
       mma_commit_warp(&kv_empty[0]);
       for (int j = ulo; j < uhi; ++j) {
         const int itV = 2 * (j - ulo) + 1, itK1 = itV + 1;
         const bool more = j + 1 < uhi;
-        wait_slot(itV);
+        wait_group(j - ulo + 1);                         // V_j and K_{j+1}
         if (lane == 0) TRACE(12, j);
         if (active(rg[0], j)) pv(0, itV, j > rg[0].lo);
         if (lane == 0) TRACE(0, j);
-        if (more) {
-          wait_slot(itK1);
-          if (lane == 0) TRACE(15, j);
-          if (active(rg[0], j + 1)) qk(0, itK1);
-        }
+        if (more && active(rg[0], j + 1)) qk(0, itK1);
         if (lane == 0) TRACE(1, j);
         if (active(rg[1], j)) pv(1, itV, j > rg[1].lo);
         if (lane == 0) TRACE(2, j);
@@ -389,7 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int it = j - R.lo;
       if (wq == 0 && lane == 0) TRACE(4 + 4 * t, j);
-      mbar_wait(&s_full[t], it & 1);
+      WAIT_SM(&s_full[t], it & 1);
       tc_fence_after();
       if (wq == 0 && lane == 0) TRACE(5 + 4 * t, j);
       float x[BN];
@@ -422,7 +431,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       l *= alpha;                                       // xsum = h(xsum) + ...
       // exp(x - m), local sum, P -> bf16 into TMEM (aliasing S)
       const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
-      if (kToken) named_bar_sync(t == 0 ? kBarTok0 : kBarTok1, 256);   // acquire the exp token
+      float m_use_t = m_use;
+      if (kToken) {
+        named_bar_sync(t == 0 ? kBarTok0 : kBarTok1, 256);   // acquire the exp token
+#ifdef ATTN_TOKEN_STRICT
+        asm volatile("" : "+f"(m_use_t));   // the exponentials below cannot be hoisted above the acquire
+#endif
+      }
       if (wq == 0 && lane == 0) TRACE(6 + 4 * t, j);
       float sum0 = 0.f, sum1 = 0.f;
 #pragma unroll
@@ -432,11 +447,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int e = 0; e < 16; ++e) {
           float a0, a1;
           if constexpr (kPlain) {
-            a0 = fmaf(x[c0 + 2 * e], v.scale_log2, -m_use);
-            a1 = fmaf(x[c0 + 2 * e + 1], v.scale_log2, -m_use);
+            a0 = fmaf(x[c0 + 2 * e], v.scale_log2, -m_use_t);
+            a1 = fmaf(x[c0 + 2 * e + 1], v.scale_log2, -m_use_t);
           } else {
-            a0 = x[c0 + 2 * e] - m_use;
-            a1 = x[c0 + 2 * e + 1] - m_use;
+            a0 = x[c0 + 2 * e] - m_use_t;
+            a1 = x[c0 + 2 * e + 1] - m_use_t;
           }
           float p0, p1;
           if (ATTN_POLY_DIV > 0 && (e % (ATTN_POLY_DIV > 0 ? ATTN_POLY_DIV : 1)) == (ATTN_POLY_DIV > 0 ? ATTN_POLY_DIV : 1) - 1) {
@@ -452,6 +467,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tmem_st16(tS + c0 / 2, pk);
       }
+#ifdef ATTN_TOKEN_STRICT
+      if (kToken) asm volatile("" ::"f"(sum0), "f"(sum1));   // all exponentials done before the release
+#endif
       if (kToken) {                                         // release the token
         if (t == 0) named_bar_arrive(kBarTok1, 256);
         else if (j + 1 < uhi) named_bar_arrive(kBarTok0, 256);
@@ -478,9 +496,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_st_wait();
       l += sum;
       tc_fence_before();
-      __syncwarp();
       if (t == 0 && lane == 0) TRACE(20 + wq, j);
-      if (lane == 0) mbar_arrive(&p_ready[t]);
+      named_bar_arrive(kBarP0 + t, 160);          // P_t(j) in TMEM -> MMA issuer
     }
 
     // ------------------------------------------------------------ epilogue: O / l -> bf16 -> TMA store
