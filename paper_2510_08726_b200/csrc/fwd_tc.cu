@@ -36,8 +36,19 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BN = 128;
-constexpr int kThreads = 384;
-constexpr int kWarpLoad = 8, kWarpMma = 9, kWarpAlloc = 10;
+#ifndef ATTN_ROW_SPLIT
+#define ATTN_ROW_SPLIT 1
+#endif
+// Threads per S row: 2 => each row's 128 columns are split between two warps
+// (same TMEM lanes, different columns); row max and sum are exchanged through
+// shared memory.  Measured equal to 1 thread per row on B200 (a tile's 16K
+// exponentials are bound by the SM's 16 ex2/clk either way), so 1 is default.
+constexpr int kHalves = ATTN_ROW_SPLIT;
+constexpr int kTileThreads = 128 * kHalves;            // softmax threads per query tile
+constexpr int kSoftmaxWarps = 2 * kTileThreads / 32;
+constexpr int kWarpLoad = kSoftmaxWarps, kWarpMma = kSoftmaxWarps + 1, kWarpAlloc = kSoftmaxWarps + 2;
+constexpr int kThreads = (kSoftmaxWarps + 3) * 32;
+constexpr int kHC = BN / kHalves;                       // S columns per softmax thread
 #ifndef ATTN_PREFETCH
 #define ATTN_PREFETCH 0
 #endif
@@ -46,7 +57,8 @@ constexpr float kTau = 8.0f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr uint32_t kBarTok0 = 3, kBarTok1 = 4;   // named barriers of the exp token
-constexpr uint32_t kBarP0 = 5;                    // 5 / 6: "P_t ready" (128 softmax threads + MMA warp)
+constexpr uint32_t kBarP0 = 5;                    // 5 / 6: "P_t ready" (softmax threads of tile t + MMA warp)
+constexpr uint32_t kBarX0 = 7;                    // 7 / 8: row-max / row-sum exchange between column halves
 #ifndef ATTN_TOKEN
 #define ATTN_TOKEN 1
 #endif
@@ -94,10 +106,11 @@ struct Cfg {
   static constexpr int kSmemQ = 2 * kQTileBytes;
   static constexpr int kSmemKV = kStages * kKVTileBytes;
   static constexpr int kNumBars = 1 + 2 * kStages + 6;
+  static constexpr int kXchgBytes = kHalves > 1 ? 2 * kHalves * BM * 4 : 0;   // [tile][half][row] floats
 #ifdef ATTN_TRACE
-  static constexpr int kSmemBytes = 1024 + kSmemQ + kSmemKV + 1024 + 26 * 40 * 8;
+  static constexpr int kSmemBytes = kSmemQ + kSmemKV + kXchgBytes + 1024 + 26 * 40 * 8;
 #else
-  static constexpr int kSmemBytes = 1024 + kSmemQ + kSmemKV + kNumBars * 8 + 16;
+  static constexpr int kSmemBytes = kSmemQ + kSmemKV + kXchgBytes + kNumBars * 8 + 16;
 #endif
 };
 
@@ -172,12 +185,12 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
 // log2 domain used by the exponentials; returns the row max of the tile.
 // Plain variant: x stays raw (scale folded into the exp FFMA) and the max is
 // rescaled afterwards (scale > 0 so max commutes with it).
-template <bool kAlibi, bool kSoftcap, bool kMask>
-__device__ __forceinline__ float score_tile(float (&x)[BN], const VariantParams& v, float nslope2, float dq0,
+template <bool kAlibi, bool kSoftcap, bool kMask, int N>
+__device__ __forceinline__ float score_tile(float (&x)[N], const VariantParams& v, float nslope2, float dq0,
                                             int rel_lo, int rel_hi) {
   float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};   // independent chains for ILP
 #pragma unroll
-  for (int c = 0; c < BN; ++c) {
+  for (int c = 0; c < N; ++c) {
     float xv = x[c];
     if constexpr (kSoftcap) {
       xv = v.softcap_log2 * tanh_approx(xv * v.scale_over_cap);   // R3: cap * tanh(x / cap)
@@ -201,11 +214,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                   const VariantParams v, float* __restrict__ lse) {
   using C = Cfg<D>;
   constexpr bool kPlain = !kAlibi && !kSoftcap;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // The 128-byte swizzle needs 1024-byte aligned tiles; dynamic shared memory
+  // starts at offset 0 of the CTA's window (no static shared memory here).
+  if ((smem_u32(smem_raw) & 1023) != 0) __trap();
+  uint8_t* smem = smem_raw;
   uint8_t* sQ = smem;
   uint8_t* sKV = smem + C::kSmemQ;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::kSmemKV);
+  float* xchg = reinterpret_cast<float*>(sKV + C::kSmemKV);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::kSmemKV + C::kXchgBytes);
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;
   uint64_t* kv_empty = kv_full + C::kStages;
@@ -214,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* o_done = p_ready + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 #ifdef ATTN_TRACE
-  long long* s_trace = reinterpret_cast<long long*>(smem + C::kSmemQ + C::kSmemKV + 1024);
+  long long* s_trace = reinterpret_cast<long long*>(smem + C::kSmemQ + C::kSmemKV + C::kXchgBytes + 1024);
   if (trace_cta())
     for (int i = threadIdx.x; i < kTrEv * kTrSteps; i += blockDim.x) s_trace[i] = 0;
 #endif
@@ -334,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit_warp(&s_full[t]);
       };
       auto pv = [&](int t, int it, bool acc) {   // O_t += P_t V (P straight from TMEM)
-        named_bar_sync(kBarP0 + t, 160);          // the 128 softmax threads of tile t arrived
+        named_bar_sync(kBarP0 + t, kTileThreads + 32);   // the softmax threads of tile t arrived
         tc_fence_after();
         if (lane == 0) TRACE(13 + t, it / 2);
         const uint32_t sv = smem_u32(sKV + (it % C::kStages) * C::kKVTileBytes);
@@ -367,55 +384,69 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp < 8) {
+  } else if (warp < kSoftmaxWarps) {
     // ------------------------------------------------------------ softmax / correction / epilogue
-    const int t = (int)warp >> 2;
-    const int wq = warp & 3;
+    // Thread (tile t, row r, column half h) owns S columns [h*kHC, (h+1)*kHC) of row r.
+    const int t = (int)warp / (kSoftmaxWarps / 2);
+    const int wt = (int)warp % (kSoftmaxWarps / 2);       // warp within the tile
+    const int half = wt >> 2;
+    const int wq = warp & 3;                               // TMEM lane quarter
     const int r = wq * 32 + lane;
+    const int tid_t = wt * 32 + lane;                      // thread index within the tile
     const Range R = t == 0 ? rng0 : rng1;
     const int i = row0 + t * BM + r;
     const long long qpos = v.q_off + i;
     int jlo_row, jhi_row;
     row_bounds(s, v, qpos, jlo_row, jhi_row);
     const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
-    const uint32_t tS = tmem + t * 128 + lane_off;
-    const uint32_t tO = tmem + 256 + t * 128 + lane_off;
+    const int c_base = half * kHC;                         // first S column of this thread
+    constexpr int kOC = D / kHalves;                       // O columns of this thread
+    const uint32_t tS = tmem + t * 128 + lane_off + c_base;
+    const uint32_t tP = tmem + t * 128 + lane_off + half * (kHC / 2);   // bf16 pairs, aliasing S
+    const uint32_t tO = tmem + 256 + t * 128 + lane_off + half * kOC;
+    float* my_x = xchg + (t * kHalves + half) * BM + r;             // exchange slots (kHalves == 2)
+    const float* other_x = xchg + (t * kHalves + (1 - half)) * BM + r;
     const float nslope2 = kAlibi ? -v.alibi[hq] * kLog2e : 0.f;
     float m_ref = -INFINITY;  // stale reference max (log2 units), R9
-    float l = 0.f;            // running denominator (sum of un-rounded fp32 p, R10)
+    float l = 0.f;            // running denominator over this thread's columns (un-rounded fp32 p, R10)
 
-    // Ping-pong: the exp phases of the two warpgroups alternate in KV-tile order
-    // (token passed through named barriers 3/4), so one tile's softmax always
-    // runs under the other tile's MMAs instead of both contending for MUFU.
-    if (kToken && t == 1 && uhi > ulo) named_bar_arrive(kBarTok0, 256);
+    // Ping-pong: the exp phases of the two tiles alternate in KV-tile order
+    // (token passed through named barriers 3/4).
+    if (kToken && t == 1 && uhi > ulo) named_bar_arrive(kBarTok0, 2 * kTileThreads);
     for (int j = ulo; j < uhi; ++j) {
-      if (!active(R, j)) {   // keep the token moving through tiles this warpgroup skips
+      if (!active(R, j)) {   // keep the token moving through tiles this tile skips
         if (!kToken) continue;
-        named_bar_sync(t == 0 ? kBarTok0 : kBarTok1, 256);
-        if (t == 0) named_bar_arrive(kBarTok1, 256);
-        else if (j + 1 < uhi) named_bar_arrive(kBarTok0, 256);
+        named_bar_sync(t == 0 ? kBarTok0 : kBarTok1, 2 * kTileThreads);
+        if (t == 0) named_bar_arrive(kBarTok1, 2 * kTileThreads);
+        else if (j + 1 < uhi) named_bar_arrive(kBarTok0, 2 * kTileThreads);
         continue;
       }
       const int it = j - R.lo;
-      if (wq == 0 && lane == 0) TRACE(4 + 4 * t, j);
+      if (tid_t == 0) TRACE(4 + 4 * t, j);
       WAIT_SM(&s_full[t], it & 1);
       tc_fence_after();
-      if (wq == 0 && lane == 0) TRACE(5 + 4 * t, j);
-      float x[BN];
+      if (tid_t == 0) TRACE(5 + 4 * t, j);
+      float x[kHC];
       {
-        uint32_t u[BN];
+        uint32_t u[kHC];
 #pragma unroll
-        for (int c = 0; c < BN / 32; ++c) tmem_ld32(tS + c * 32, reinterpret_cast<uint32_t(&)[32]>(u[c * 32]));
+        for (int c = 0; c < kHC / 32; ++c) tmem_ld32(tS + c * 32, reinterpret_cast<uint32_t(&)[32]>(u[c * 32]));
         tmem_ld_wait();
 #pragma unroll
-        for (int c = 0; c < BN; ++c) x[c] = u2f(u[c]);
+        for (int c = 0; c < kHC; ++c) x[c] = u2f(u[c]);
       }
       // Fig. 19 max_local (+ score_mod, mask) -> max_global
       const bool need_mask = !(j * BN >= R.jlo_last && (j + 1) * BN - 1 <= R.jhi_first);
-      const int rel_lo = jlo_row - j * BN, rel_hi = jhi_row - j * BN;
-      const float dq0 = (float)(qpos - v.kv_off - (long long)j * BN);
-      const float mt = need_mask ? score_tile<kAlibi, kSoftcap, true>(x, v, nslope2, dq0, rel_lo, rel_hi)
-                                 : score_tile<kAlibi, kSoftcap, false>(x, v, nslope2, dq0, rel_lo, rel_hi);
+      const int rel_lo = jlo_row - j * BN - c_base, rel_hi = jhi_row - j * BN - c_base;
+      const float dq0 = (float)(qpos - v.kv_off - (long long)j * BN - c_base);
+      float mt = need_mask ? score_tile<kAlibi, kSoftcap, true>(x, v, nslope2, dq0, rel_lo, rel_hi)
+                           : score_tile<kAlibi, kSoftcap, false>(x, v, nslope2, dq0, rel_lo, rel_hi);
+      if constexpr (kHalves > 1) {
+        // both halves must have loaded S before either overwrites it with P (P aliases S)
+        *my_x = mt;
+        named_bar_sync(kBarX0 + t, kTileThreads);
+        mt = fmaxf(mt, *other_x);
+      }
       const float m_run = fmaxf(m_ref, mt);
       bool move, need_o;
       if (m_ref == -INFINITY) {
@@ -433,15 +464,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
       float m_use_t = m_use;
       if (kToken) {
-        named_bar_sync(t == 0 ? kBarTok0 : kBarTok1, 256);   // acquire the exp token
+        named_bar_sync(t == 0 ? kBarTok0 : kBarTok1, 2 * kTileThreads);   // acquire the exp token
 #ifdef ATTN_TOKEN_STRICT
-        asm volatile("" : "+f"(m_use_t));   // the exponentials below cannot be hoisted above the acquire
+        asm volatile("" : "+f"(m_use_t));
 #endif
       }
-      if (wq == 0 && lane == 0) TRACE(6 + 4 * t, j);
+      if (tid_t == 0) TRACE(6 + 4 * t, j);
       float sum0 = 0.f, sum1 = 0.f;
 #pragma unroll
-      for (int c0 = 0; c0 < BN; c0 += 32) {
+      for (int c0 = 0; c0 < kHC; c0 += 32) {
         uint32_t pk[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
@@ -465,25 +496,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           sum1 += p1;
           pk[e] = pack2<kF16>(p0, p1);
         }
-        tmem_st16(tS + c0 / 2, pk);
+        tmem_st16(tP + c0 / 2, pk);
       }
 #ifdef ATTN_TOKEN_STRICT
-      if (kToken) asm volatile("" ::"f"(sum0), "f"(sum1));   // all exponentials done before the release
+      if (kToken) asm volatile("" ::"f"(sum0), "f"(sum1));
 #endif
       if (kToken) {                                         // release the token
-        if (t == 0) named_bar_arrive(kBarTok1, 256);
-        else if (j + 1 < uhi) named_bar_arrive(kBarTok0, 256);
+        if (t == 0) named_bar_arrive(kBarTok1, 2 * kTileThreads);
+        else if (j + 1 < uhi) named_bar_arrive(kBarTok0, 2 * kTileThreads);
       }
       const float sum = sum0 + sum1;
-      if (wq == 0 && lane == 0) TRACE(7 + 4 * t, j);
-      if (t == 0 && lane == 0) TRACE(16 + wq, j);
-      // (done after P so the S registers are dead; PV(j) cannot start before p_ready)
+      if (tid_t == 0) TRACE(7 + 4 * t, j);
+      if (t == 0 && lane == 0 && wt < 4) TRACE(16 + wq, j);
+      // (done after P so the S registers are dead; PV(j) cannot start before P is ready)
       if (__any_sync(0xffffffffu, need_o)) {
-        // O = h(O): wait for PV of the previous tile, then rescale the TMEM accumulator.
+        // O = h(O): wait for PV of the previous tile, then rescale this thread's O columns.
         mbar_wait(&o_done[t], (it - 1) & 1);
         tc_fence_after();
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
+        for (int c = 0; c < kOC / 32; ++c) {
           uint32_t o[32];
           tmem_ld32(tO + c * 32, o);
           tmem_ld_wait();
@@ -496,14 +527,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_st_wait();
       l += sum;
       tc_fence_before();
-      if (t == 0 && lane == 0) TRACE(20 + wq, j);
-      named_bar_arrive(kBarP0 + t, 160);          // P_t(j) in TMEM -> MMA issuer
+      if (t == 0 && lane == 0 && wt < 4) TRACE(20 + wq, j);
+      named_bar_arrive(kBarP0 + t, kTileThreads + 32);   // P_t(j) in TMEM -> MMA issuer
     }
 
-    // ------------------------------------------------------------ epilogue: O / l -> bf16 -> TMA store
+    // ------------------------------------------------------------ epilogue: O / l -> 16-bit -> TMA store
     const int n_it = R.hi - R.lo;
     const bool tile_rows = (row0 + t * BM) < s.Sq;
     if (tile_rows) {
+      if constexpr (kHalves > 1) {   // total row sum = both halves' partial sums
+        named_bar_sync(kBarX0 + t, kTileThreads);   // partners are done reading the max slots
+        *my_x = l;
+        named_bar_sync(kBarX0 + t, kTileThreads);
+        l += *other_x;
+      }
       if (n_it > 0) {
         mbar_wait(&o_done[t], (n_it - 1) & 1);
         tc_fence_after();
@@ -513,7 +550,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float inv_l = l > 0.f ? 1.f / l : 0.f;
       uint8_t* sOut = sQ + t * C::kQTileBytes;
 #pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
+      for (int c = 0; c < kOC / 32; ++c) {
         uint32_t o[32];
         if (n_it > 0) {
           tmem_ld32(tO + c * 32, o);
@@ -525,22 +562,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t pk[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) pk[e] = pack2<kF16>(u2f(o[2 * e]) * inv_l, u2f(o[2 * e + 1]) * inv_l);
-        uint8_t* rowp = sOut + (c >> 1) * (BM * 128) + r * 128;
+        const int cg = half * (kOC / 32) + c;               // 32-column chunk of the O row
+        uint8_t* rowp = sOut + (cg >> 1) * (BM * 128) + r * 128;
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
-          const int ch = (c & 1) * 4 + q4;
+          const int ch = (cg & 1) * 4 + q4;
           *reinterpret_cast<uint4*>(rowp + ((ch ^ (r & 7)) << 4)) =
               make_uint4(pk[4 * q4], pk[4 * q4 + 1], pk[4 * q4 + 2], pk[4 * q4 + 3]);
         }
       }
       fence_proxy_async_smem();
-      named_bar_sync(1 + t, 128);
-      if (wq == 0 && lane == 0) {
+      named_bar_sync(1 + t, kTileThreads);
+      if (tid_t == 0) {
         for (int bx = 0; bx < C::kBoxes; ++bx) tma_store_4d(&tm_o, sOut + bx * BM * 128, bx * 64, row0 + t * BM, hq, b);
         bulk_commit();
         bulk_wait_read0();
       }
-      if (lse != nullptr && i < s.Sq)
+      if (lse != nullptr && i < s.Sq && half == 0)
         lse[((size_t)b * s.Hq + hq) * s.Sq + i] = l > 0.f ? m_ref * kLn2 + logf(l) : -INFINITY;
     }
   }
