@@ -180,6 +180,28 @@ ATTN_API attn_status attn_combine(int32_t batch, int32_t heads, int32_t head_dim
                          attn_stream_t stream);
 
 /* ---------------------------------------------------------------------
+ * attn_merge_partials -- Eq. 8 over num_parts NORMALISED partial
+ * results of the same query rows, e.g. the per-GPU outputs of a KV-sharded
+ * (context-parallel) Rolling Update prefill.  A normalised partial (O_p,
+ * lse_p) is the repaired triple (m = lse_p, l = 1, O_p) (Thm. 2: h
+ * tag-updates to any reference), so for every row:
+ *   M = max_p lse_p,  w_p = exp(lse_p - M) (0 if lse_p = -inf),
+ *   L = sum_p w_p,    O = sum_p w_p O_p / L,   lse = M + ln L
+ * (O = 0, lse = -inf if every part is empty).
+ *   o_in : DEVICE, element type in_dtype; row r of part p at
+ *          o_in + p*o_stride_part + r*o_stride_row (elements), head_dim contiguous.
+ *   lse_in: DEVICE fp32, lse_in[p*lse_stride_part + r].
+ *   o_out: DEVICE, element type out_dtype, row r at o_out + r*o_out_stride_row
+ *          (nullable);  lse_out: DEVICE fp32 [rows] (nullable).
+ * head_dim <= 256.  Errors: INVALID_ARGUMENT, UNSUPPORTED, CUDA.
+ * ------------------------------------------------------------------- */
+ATTN_API attn_status attn_merge_partials(int32_t num_parts, int64_t rows, int32_t head_dim, attn_dtype in_dtype,
+                                         const void* o_in, int64_t o_stride_part, int64_t o_stride_row,
+                                         const float* lse_in, int64_t lse_stride_part, attn_dtype out_dtype,
+                                         void* o_out, int64_t o_out_stride_row, float* lse_out,
+                                         attn_stream_t stream);
+
+/* ---------------------------------------------------------------------
  * Seeded synthetic inputs are produced by a separate library (datagen/);
  * nothing here generates data.  Introspection:
  * ------------------------------------------------------------------- */

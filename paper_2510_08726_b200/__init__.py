@@ -20,7 +20,7 @@ import torch
 from . import _ffi
 from ._ffi import AttnParts, AttnProblem, AttnTensor, check, load
 
-__all__ = ["fused_fwd", "splitkv_decode", "combine", "default_splits", "workspace_bytes",
+__all__ = ["fused_fwd", "splitkv_decode", "combine", "merge_partials", "default_splits", "workspace_bytes",
            "last_launch_count", "Parts", "load"]
 
 _DT = {torch.bfloat16: _ffi.ATTN_BF16, torch.float32: _ffi.ATTN_FP32, torch.float16: _ffi.ATTN_FP16}
@@ -212,3 +212,26 @@ def combine(parts: Parts, *, out: Optional[torch.Tensor] = None, out_dtype=torch
     if return_lse:
         return out, lse
     return out
+
+
+def merge_partials(o_parts: torch.Tensor, lse_parts: torch.Tensor, *, out: Optional[torch.Tensor] = None,
+                   out_dtype=None, return_lse: bool = False, stream=None):
+    """Eq. 8 over P normalised partials (``attn_merge_partials``):
+    o_parts [P, ..., D] (bf16/fp16/fp32), lse_parts [P, ...] fp32, with the
+    middle dimensions flattened into rows.  Returns O [..., D] (and lse)."""
+    lib = load()
+    P, D = o_parts.shape[0], o_parts.shape[-1]
+    rows = lse_parts[0].numel()
+    o2 = o_parts.reshape(P, rows, D)
+    l2 = lse_parts.reshape(P, rows)
+    if o2.stride(2) != 1 or l2.stride(1) != 1:
+        raise ValueError("partials must be contiguous over D and rows")
+    dt = o_parts.dtype if out_dtype is None else out_dtype
+    if out is None:
+        out = torch.empty(o_parts.shape[1:], dtype=dt, device=o_parts.device)
+    lse = torch.empty(lse_parts.shape[1:], dtype=torch.float32, device=o_parts.device) if return_lse else None
+    out2 = out.view(rows, D)
+    check(lib.attn_merge_partials(P, rows, D, _DT[o_parts.dtype], o2.data_ptr(), o2.stride(0), o2.stride(1),
+                                  l2.data_ptr(), l2.stride(0), _DT[out.dtype], out2.data_ptr(), out2.stride(0),
+                                  None if lse is None else lse.data_ptr(), _stream(stream)), "attn_merge_partials")
+    return (out, lse) if return_lse else out

@@ -22,7 +22,7 @@ ATTN_Q_POS_DEFAULT = -(1 << 63)
 
 EXPORTED = ("attn_fused_fwd", "attn_splitkv_default_splits", "attn_splitkv_workspace_bytes",
             "attn_splitkv_decode", "attn_combine", "attn_status_string", "attn_last_error",
-            "attn_abi_version", "attn_last_launch_count")
+            "attn_abi_version", "attn_last_launch_count", "attn_merge_partials")
 
 
 class AttnTensor(ctypes.Structure):
@@ -70,6 +70,10 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.attn_splitkv_decode.restype = ctypes.c_int
     lib.attn_combine.argtypes = [i32, i32, i32, Pa, ctypes.c_int, T, f32p, Pa, vp]
     lib.attn_combine.restype = ctypes.c_int
+    i64 = ctypes.c_int64
+    lib.attn_merge_partials.argtypes = [i32, i64, i32, ctypes.c_int, vp, i64, i64, vp, i64, ctypes.c_int, vp, i64, vp,
+                                        vp]
+    lib.attn_merge_partials.restype = ctypes.c_int
     lib.attn_status_string.argtypes = [ctypes.c_int]
     lib.attn_status_string.restype = ctypes.c_char_p
     lib.attn_last_error.restype = ctypes.c_char_p

@@ -335,4 +335,36 @@ attn_status attn_combine(int32_t batch, int32_t heads, int32_t head_dim, const a
   return st;
 }
 
+attn_status attn_merge_partials(int32_t num_parts, int64_t rows, int32_t head_dim, attn_dtype in_dtype,
+                                const void* o_in, int64_t o_stride_part, int64_t o_stride_row, const float* lse_in,
+                                int64_t lse_stride_part, attn_dtype out_dtype, void* o_out, int64_t o_out_stride_row,
+                                float* lse_out, attn_stream_t stream) {
+  g_err[0] = 0;
+  CHECK_ARG(num_parts >= 1 && rows >= 1 && head_dim >= 1, "extents must be >= 1");
+  if (head_dim > 256) return fail(ATTN_ERR_UNSUPPORTED, "merge head_dim must be <= 256");
+  CHECK_ARG(o_in != nullptr && lse_in != nullptr, "null input");
+  CHECK_ARG(o_out != nullptr || lse_out != nullptr, "no output requested");
+  auto dt_ok = [](attn_dtype d) { return d == ATTN_BF16 || d == ATTN_FP32 || d == ATTN_FP16; };
+  CHECK_ARG(dt_ok(in_dtype) && dt_ok(out_dtype), "unknown dtype");
+  attn::MergeArgs m{};
+  m.P = num_parts;
+  m.D = head_dim;
+  m.rows = rows;
+  m.in_dtype = in_dtype;
+  m.out_dtype = out_dtype;
+  m.o_in = o_in;
+  m.o_sp = o_stride_part;
+  m.o_sr = o_stride_row;
+  m.lse_in = lse_in;
+  m.l_sp = lse_stride_part;
+  m.o_out = o_out;
+  m.o_out_sr = o_out_stride_row;
+  m.lse_out = lse_out;
+  int launches = 0;
+  attn_status st = cuda_status(attn::launch_merge(m, reinterpret_cast<cudaStream_t>(stream), &launches),
+                               "merge launch");
+  if (st == ATTN_OK) g_launches = launches;
+  return st;
+}
+
 }  // extern "C"

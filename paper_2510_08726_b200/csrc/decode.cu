@@ -339,6 +339,56 @@ __global__ void __launch_bounds__(128) combine_kernel(const CombineArgs a) {
   }
 }
 
+// ---------------------------------------------------------------- Eq. 8 over normalised partials
+__device__ __forceinline__ float load_elem(const void* p, long long i, int dt) {
+  if (dt == 1) return static_cast<const float*>(p)[i];
+  if (dt == 2) return __half2float(static_cast<const __half*>(p)[i]);
+  return __bfloat162float(static_cast<const __nv_bfloat16*>(p)[i]);
+}
+__device__ __forceinline__ void store_elem(void* p, long long i, int dt, float x) {
+  if (dt == 1) static_cast<float*>(p)[i] = x;
+  else if (dt == 2) static_cast<__half*>(p)[i] = __float2half_rn(x);
+  else static_cast<__nv_bfloat16*>(p)[i] = __float2bfloat16_rn(x);
+}
+
+__global__ void __launch_bounds__(128) merge_kernel(const MergeArgs a) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long row = (long long)blockIdx.x * 4 + warp;
+  if (row >= a.rows) return;
+  float M = -INFINITY;
+  for (int p = lane; p < a.P; p += 32) M = fmaxf(M, a.lse_in[p * a.l_sp + row]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  constexpr int kMaxDL = 8;   // D <= 256
+  float acc[kMaxDL];
+#pragma unroll
+  for (int r = 0; r < kMaxDL; ++r) acc[r] = 0.f;
+  float L = 0.f;
+  if (M != -INFINITY) {
+    for (int p = 0; p < a.P; ++p) {
+      const float lp = a.lse_in[p * a.l_sp + row];
+      if (lp == -INFINITY) continue;                  // empty part: weight 0
+      const float w = expf(lp - M);                    // repair term exp(lse_p - M), l_p = 1
+      L += w;
+      const long long base = p * a.o_sp + row * a.o_sr;
+#pragma unroll
+      for (int r = 0; r < kMaxDL; ++r) {
+        const int d = lane + 32 * r;
+        if (d < a.D) acc[r] = fmaf(w, load_elem(a.o_in, base + d, a.in_dtype), acc[r]);
+      }
+    }
+  }
+  if (a.o_out) {
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+#pragma unroll
+    for (int r = 0; r < kMaxDL; ++r) {
+      const int d = lane + 32 * r;
+      if (d < a.D) store_elem(a.o_out, row * a.o_out_sr + d, a.out_dtype, acc[r] * inv);
+    }
+  }
+  if (a.lse_out && lane == 0) a.lse_out[row] = L > 0.f ? M + logf(L) : -INFINITY;
+}
+
 template <int D, bool kAlibi, bool kSoftcap, bool kF16>
 cudaError_t launch_dec_t(const DecodeArgs& a, cudaStream_t stream) {
   using C = DCfg<D>;
@@ -366,6 +416,14 @@ int decode_stage_keys(int, int) { return NK; }
 cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t stream, int* launches) {
   cudaError_t e = a.f16 ? (a.s.D == 128 ? launch_dec_d<128, true>(a, stream) : launch_dec_d<64, true>(a, stream))
                         : (a.s.D == 128 ? launch_dec_d<128, false>(a, stream) : launch_dec_d<64, false>(a, stream));
+  if (e == cudaSuccess && launches) ++*launches;
+  return e;
+}
+
+cudaError_t launch_merge(const MergeArgs& a, cudaStream_t stream, int* launches) {
+  const long long blocks = (a.rows + 3) / 4;
+  merge_kernel<<<(unsigned)blocks, 128, 0, stream>>>(a);
+  cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess && launches) ++*launches;
   return e;
 }

@@ -76,4 +76,16 @@ struct CombineArgs {
 };
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t stream, int* launches);
 
+// ------------------------------------------------------------ merge of normalised partials (Eq. 8)
+struct MergeArgs {
+  int P, D;
+  long long rows;
+  int in_dtype, out_dtype;       // 0 bf16, 1 fp32, 2 fp16 (attn_dtype values)
+  const void* o_in; long long o_sp, o_sr;
+  const float* lse_in; long long l_sp;
+  void* o_out; long long o_out_sr;
+  float* lse_out;
+};
+cudaError_t launch_merge(const MergeArgs& a, cudaStream_t stream, int* launches);
+
 }  // namespace attn

@@ -11,6 +11,11 @@
   over the W parts.  Exact because h commutes with the reducer (Eq. 4,
   P:578-579), so the merge may be grouped by split and then by rank.
 
+* Long-context prefill (context parallel, NEXT-3) shards the KV sequence the
+  same way (``prefill_kv_sharded``): every rank runs the Rolling Update kernel
+  on its keys with absolute positions, the normalised (O_r, lse_r) pairs are
+  all-gathered and merged with Eq. 8 (``attn_merge_partials``).
+
 The local section and the combine are injectable so the host-side logic can
 be tested on CPU with world_size 2 over gloo; the defaults are the CUDA
 kernels behind the C ABI.
@@ -72,3 +77,44 @@ def decode_kv_sharded(q: torch.Tensor, k_shard: torch.Tensor, v_shard: torch.Ten
     recv = torch.empty(world, B, Hq, D + 2, dtype=torch.float32, device=q.device)
     dist.all_gather_into_tensor(recv, send, group=group)
     return final(Parts.packed(recv), q.dtype, return_lse)
+
+
+# ----------------------------------------------------------------------------- context-parallel prefill (NEXT-3)
+def _prefill_local(q, k_shard, v_shard, *, kv_pos_offset, seqlen_kv_total, variant):
+    from . import fused_fwd
+    return fused_fwd(q, k_shard, v_shard, kv_pos_offset=kv_pos_offset, seqlen_kv_total=seqlen_kv_total,
+                     return_lse=True, **variant)
+
+
+def prefill_kv_sharded(q: torch.Tensor, k_shard: torch.Tensor, v_shard: torch.Tensor, *, kv_pos_offset: int,
+                       seqlen_kv_total: int, group=None, out_dtype=None, local: Optional[Callable] = None,
+                       final: Optional[Callable] = None, **variant):
+    """Context-parallel (KV-sharded) Rolling Update prefill: every rank holds all
+    queries and keys [kv_pos_offset, kv_pos_offset + L_r) of a sequence of
+    seqlen_kv_total keys.  Each rank runs the fused forward on its shard (the
+    mask uses absolute positions), the (O_r, lse_r) pairs are all-gathered and
+    merged with the Eq. 8 combine (the paper's rolling update composed with
+    privatisation, Fig. 19, lifted to GPUs).  Returns O [B, H, Sq, D] (and lse
+    [B, H, Sq]) on every rank."""
+    local = local or _prefill_local
+    world = dist.get_world_size(group)
+    B, H, S, D = q.shape
+    o_r, lse_r = local(q, k_shard, v_shard, kv_pos_offset=kv_pos_offset, seqlen_kv_total=seqlen_kv_total,
+                       variant=variant)
+    # gathered along dim 0 ([W*B, ...]; gloo requires it), then viewed as [W, B, ...]
+    o_all = torch.empty((world * B,) + tuple(o_r.shape[1:]), dtype=o_r.dtype, device=o_r.device)
+    lse_all = torch.empty((world * B,) + tuple(lse_r.shape[1:]), dtype=lse_r.dtype, device=o_r.device)
+    dist.all_gather_into_tensor(o_all, o_r.contiguous(), group=group)
+    dist.all_gather_into_tensor(lse_all, lse_r.contiguous(), group=group)
+    o_all = o_all.view((world,) + tuple(o_r.shape))
+    lse_all = lse_all.view((world,) + tuple(lse_r.shape))
+    return merge_prefill_parts(o_all, lse_all, out_dtype or q.dtype, final=final)
+
+
+def merge_prefill_parts(o_all: torch.Tensor, lse_all: torch.Tensor, out_dtype, final: Optional[Callable] = None):
+    """Eq. 8 over W normalised partials o_all [W, B, H, S, D], lse_all [W, B, H, S]
+    (a normalised (O, lse) is the repaired triple (m = lse, l = 1, O))."""
+    if final is not None:
+        return final(o_all, lse_all, out_dtype)
+    from . import merge_partials
+    return merge_partials(o_all, lse_all, out_dtype=out_dtype, return_lse=True)

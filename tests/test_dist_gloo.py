@@ -89,3 +89,46 @@ def test_kv_sharded_decode_two_ranks(tmp_path):
         lse = np.load(tmp_path / f"lse{r}.npy")
         np.testing.assert_allclose(out, ref_o, atol=2e-6)       # fp32 gather of fp64 partials
         np.testing.assert_allclose(lse, ref_l[:, :, 0], atol=2e-6)
+
+
+def _prefill_local_oracle(q, k_shard, v_shard, *, kv_pos_offset, seqlen_kv_total, variant):
+    """Stand-in for the Rolling Update kernel on one KV shard: oracle O and lse."""
+    Bq, Hq_, S, Dd = q.shape
+    p = oracle.Problem(Bq, Hq_, k_shard.shape[1], S, k_shard.shape[2], Dd, scale=1 / math.sqrt(Dd), causal=True,
+                       kv_pos_offset=kv_pos_offset, seqlen_kv_total=seqlen_kv_total)
+    o, lse = oracle.attention(p, q.numpy(), k_shard.numpy(), v_shard.numpy())
+    return torch.tensor(o), torch.tensor(lse)
+
+
+def _prefill_final_oracle(o_all, lse_all, out_dtype):
+    o, l = o_all.numpy(), lse_all.numpy()
+    live = np.isfinite(l)
+    out, lse = oracle.splitk_combine(np.where(live, l, -np.inf), live.astype(float), o)
+    return torch.tensor(out), torch.tensor(lse)
+
+
+def _cp_worker(rank, world, port, result_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    S = 57
+    q = datagen.as_f64(datagen.tensor(12, 1, (1, 2, S, 8)), "bf16")
+    k = datagen.as_f64(datagen.tensor(12, 2, (1, 2, S, 8)), "bf16")
+    v = datagen.as_f64(datagen.tensor(12, 3, (1, 2, S, 8)), "bf16")
+    lo, hi = pdist.shard_range(S, rank, world)
+    out, lse = pdist.prefill_kv_sharded(torch.tensor(q), torch.tensor(k[:, :, lo:hi]), torch.tensor(v[:, :, lo:hi]),
+                                        kv_pos_offset=lo, seqlen_kv_total=S, local=_prefill_local_oracle,
+                                        final=_prefill_final_oracle)
+    np.save(os.path.join(result_dir, f"cp{rank}.npy"), out.numpy())
+    dist.destroy_process_group()
+
+
+def test_kv_sharded_prefill_two_ranks(tmp_path):
+    port = 29400 + os.getpid() % 100
+    mp.spawn(_cp_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    S = 57
+    q = datagen.as_f64(datagen.tensor(12, 1, (1, 2, S, 8)), "bf16")
+    k = datagen.as_f64(datagen.tensor(12, 2, (1, 2, S, 8)), "bf16")
+    v = datagen.as_f64(datagen.tensor(12, 3, (1, 2, S, 8)), "bf16")
+    ref, _ = oracle.attention(oracle.Problem(1, 2, 2, S, S, 8, scale=1 / math.sqrt(8), causal=True), q, k, v)
+    for r in range(2):
+        np.testing.assert_allclose(np.load(tmp_path / f"cp{r}.npy"), ref, atol=1e-12)

@@ -60,3 +60,67 @@ def test_kv_sharded_decode_nccl_one_rank():
     finally:
         if created:
             dist.destroy_process_group()
+
+
+# --------------------------------------------------------------------------- context-parallel prefill (NEXT-3)
+@pytest.mark.parametrize("W,variant", [(2, dict(causal=True)), (3, dict(causal=True, window_left=300)),
+                                       (4, dict())])
+def test_kv_sharded_prefill_loopback(W, variant):
+    B, Hq, Hkv, S, D = 1, 4, 2, 700, 128
+    kw = dict(variant)
+    p = problem(B, Hq, Hkv, S, S, D, **kw)
+    raw, f64 = gen_qkv(1200 + W, B, Hq, Hkv, S, S, D)
+    ref_o, ref_l = oracle.attention(p, *f64)
+    q, k, v = (dgd.to_device(x) for x in raw)
+    win = (kw.pop("window_left", -1), -1)
+    o_all = torch.empty(W, B, Hq, S, D, dtype=torch.bfloat16, device="cuda")
+    lse_all = torch.empty(W, B, Hq, S, device="cuda")
+    for r in range(W):
+        lo, hi = pdist.shard_range(S, r, W)
+        o_r, l_r = pdist._prefill_local(q, k[:, :, lo:hi].contiguous(), v[:, :, lo:hi].contiguous(),
+                                        kv_pos_offset=lo, seqlen_kv_total=S, variant=dict(window=win, **kw))
+        o_all[r].copy_(o_r)
+        lse_all[r].copy_(l_r)
+    out, lse = pdist.merge_prefill_parts(o_all, lse_all, torch.bfloat16)
+    assert_bf16_close(out.float().cpu().numpy().astype(np.float64), ref_o, f"CP prefill W={W}")
+    assert_lse_close(lse.cpu().numpy(), ref_l, LSE_TOL_BF16, "CP lse")
+
+
+def test_merge_partials_matches_oracle():
+    """attn_merge_partials on oracle-made normalised partials, incl. empty (-inf) parts."""
+    P, R, D = 5, 37, 64
+    rng = np.random.default_rng(5)
+    m = rng.standard_normal((P, R)) * 2
+    l = rng.uniform(0.5, 20, (P, R))
+    o = rng.standard_normal((P, R, D)) * l[..., None]
+    m[1, :10] = -np.inf
+    l[1, :10] = 0
+    o[1, :10] = 0
+    ref_o, ref_l = oracle.splitk_combine(m, l, o)
+    live = np.isfinite(m)
+    lse_p = np.where(live, m + np.log(np.where(live, l, 1.0)), -np.inf)
+    o_norm = np.where(live[..., None], o / np.where(live, l, 1.0)[..., None], 0.0)
+    out, lse = pb.merge_partials(torch.tensor(o_norm, dtype=torch.float32, device="cuda"),
+                                 torch.tensor(lse_p, dtype=torch.float32, device="cuda"), return_lse=True)
+    np.testing.assert_allclose(out.cpu().numpy(), ref_o, rtol=1e-5, atol=1e-5)
+    np.testing.assert_allclose(lse.cpu().numpy(), ref_l, rtol=1e-5, atol=1e-5)
+
+
+def test_kv_sharded_prefill_nccl_one_rank():
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", str(29900 + os.getpid() % 90))
+    created = False
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+        created = True
+    try:
+        B, Hq, Hkv, S, D = 1, 2, 2, 300, 64
+        p = problem(B, Hq, Hkv, S, S, D, causal=True)
+        raw, f64 = gen_qkv(88, B, Hq, Hkv, S, S, D)
+        ref_o, _ = oracle.attention(p, *f64)
+        q, k, v = (dgd.to_device(x) for x in raw)
+        out, _ = pdist.prefill_kv_sharded(q, k, v, kv_pos_offset=0, seqlen_kv_total=S, causal=True)
+        assert_bf16_close(out.float().cpu().numpy().astype(np.float64), ref_o, "CP nccl 1 rank")
+    finally:
+        if created:
+            dist.destroy_process_group()
