@@ -368,6 +368,28 @@ def main_gpu(args):
                          "algorithmic_bytes_per_launch": 2.0 * Bd * Hkvd * L * Dd * 2 / world},
         }
 
+    # ------------------------------------------------------------- NEXT-4: Fig. 2 reduction chain (softmax rows)
+    if not args.no_softmax:
+        rows, cols = 65536, 4096
+        xs = torch.empty(rows, cols, dtype=torch.bfloat16, device=dev)
+        dgd.fill_(xs, datagen.config_seed(6), 1, start=rank * xs.numel())
+        ys = torch.empty_like(xs)
+        sstep = lambda: pb.softmax_rows(xs, out=ys)  # noqa: E731
+        sstep()
+        torch.cuda.synchronize()
+        sms, sclk = timed(sstep, max(args.steps, 20), args.warmup)
+        sbytes = 2.0 * rows * cols * 2          # read x once + write y once
+        sgbs = sbytes / (sms * 1e-3) / 1e9
+        line["softmax_rows"] = {
+            "metric": "Fig. 2 chain (row max, row sum, softmax) HBM GB/s (x read + y write)", "value": world * sgbs,
+            "unit": "GB/s", "ms_per_step": sms, "scaling": "weak" if world > 1 else None,
+            "config": {"workload": "softmax rows (NEXT-4)", "rows": rows, "cols": cols, "dtype": "bf16"},
+            "roofline": {"bound": "hbm", "achieved": sgbs, "peak": peaks["hbm"], "unit": "GB/s",
+                         "frac": sgbs / peaks["hbm"], "traffic": None, "kernel": "softmax_rows_kernel",
+                         "algorithmic_bytes_per_launch": sbytes},
+        }
+        del xs, ys
+
     # ------------------------------------------------------------- CPU baseline (oracle), rank 0, N = 1
     if rank == 0 and world == 1 and not args.no_cpu:
         rate, heads, secs = oracle_sample_rate(name, budget_s=args.cpu_budget)
@@ -399,6 +421,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-softmax", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()
     if args.warmup < 3:

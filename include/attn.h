@@ -202,6 +202,23 @@ ATTN_API attn_status attn_merge_partials(int32_t num_parts, int64_t rows, int32_
                                          attn_stream_t stream);
 
 /* ---------------------------------------------------------------------
+ * attn_softmax_rows -- the paper's motivating reduction chain (Fig. 2,
+ * P:164-215) on a [rows][cols] matrix, fused into one pass with both repairs
+ * (privatised local reductions rolled across chunks, Fig. 19 / Fig. 2c, then
+ * the Eq. 8 merge across threads):
+ *   row_max[r] = max_j x[r][j]                (natural units; -inf if empty)
+ *   row_sum[r] = sum_j exp(x[r][j] - row_max[r])   (Fig. 2a's xsum; 0 if empty)
+ *   y[r][j]    = exp(x[r][j] - row_max[r]) / row_sum[r]   (0 for an empty row)
+ * x, y: DEVICE, element type dtype, row stride in elements, contiguous rows;
+ * base 16-byte aligned and stride a multiple of 16 bytes.  y, row_max,
+ * row_sum are each nullable (at least one set).  Errors: INVALID_ARGUMENT,
+ * ALIGNMENT, CUDA.
+ * ------------------------------------------------------------------- */
+ATTN_API attn_status attn_softmax_rows(int64_t rows, int32_t cols, attn_dtype dtype, const void* x,
+                                       int64_t x_stride_row, void* y, int64_t y_stride_row, float* row_max,
+                                       float* row_sum, attn_stream_t stream);
+
+/* ---------------------------------------------------------------------
  * Seeded synthetic inputs are produced by a separate library (datagen/);
  * nothing here generates data.  Introspection:
  * ------------------------------------------------------------------- */

@@ -29,4 +29,5 @@ from .softmax_chain import (  # noqa: F401
     softmax_denominator_privatized,
     softmax_denominator_splitk,
     repair_h,
+    softmax_rows,
 )

@@ -117,3 +117,18 @@ def softmax_denominator_splitk(inp: np.ndarray, split: int):
         for j0 in range(nsplit):                                           # s_sum_global
             sum_g[i] += math.exp(max_l[i, j0] - max_g[i]) * sum_l[i, j0]
     return max_g, sum_g
+
+
+def softmax_rows(inp: np.ndarray):
+    """Fig. 2a vectorised over rows in fp64 (the DEFINITION the softmax-rows
+    kernel is checked against): xmax = max_j inp, xsum = sum_j exp(inp - xmax),
+    plus the normalised softmax y = exp(inp - xmax) / xsum.  A row that is all
+    -inf gives xmax = -inf, xsum = 0, y = 0 (reading R8)."""
+    x = np.asarray(inp, dtype=np.float64)
+    xmax = x.max(axis=1)
+    live = xmax > -np.inf
+    e = np.exp(x - np.where(live, xmax, 0.0)[:, None])            # s_exp, exp(-inf) = 0
+    xsum = e.sum(axis=1)                                           # s_sum
+    with np.errstate(invalid="ignore", divide="ignore"):
+        y = np.where(live[:, None], e / np.where(live, xsum, 1.0)[:, None], 0.0)
+    return xmax, xsum, y

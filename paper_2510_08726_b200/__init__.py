@@ -20,7 +20,7 @@ import torch
 from . import _ffi
 from ._ffi import AttnParts, AttnProblem, AttnTensor, check, load
 
-__all__ = ["fused_fwd", "splitkv_decode", "combine", "merge_partials", "default_splits", "workspace_bytes",
+__all__ = ["fused_fwd", "splitkv_decode", "combine", "merge_partials", "softmax_rows", "default_splits", "workspace_bytes",
            "last_launch_count", "Parts", "load"]
 
 _DT = {torch.bfloat16: _ffi.ATTN_BF16, torch.float32: _ffi.ATTN_FP32, torch.float16: _ffi.ATTN_FP16}
@@ -235,3 +235,30 @@ def merge_partials(o_parts: torch.Tensor, lse_parts: torch.Tensor, *, out: Optio
                                   l2.data_ptr(), l2.stride(0), _DT[out.dtype], out2.data_ptr(), out2.stride(0),
                                   None if lse is None else lse.data_ptr(), _stream(stream)), "attn_merge_partials")
     return (out, lse) if return_lse else out
+
+
+def softmax_rows(x: torch.Tensor, *, out: Optional[torch.Tensor] = None, want_out: bool = True,
+                 return_stats: bool = False, stream=None):
+    """The Fig. 2 reduction chain (``attn_softmax_rows``) on a [rows, cols] tensor:
+    softmax y, and with ``return_stats`` the row max and Fig. 2a's row sum
+    sum exp(x - max)."""
+    lib = load()
+    if x.dim() != 2 or x.stride(1) != 1:
+        raise ValueError("x must be [rows, cols] with contiguous columns")
+    rows, cols = x.shape
+    y = None
+    if want_out:
+        if out is None:   # rows padded to a 16-byte multiple (the kernel's vector alignment)
+            per16 = 16 // x.element_size()
+            y = torch.empty(rows, -(-cols // per16) * per16, dtype=x.dtype, device=x.device)[:, :cols]
+        else:
+            y = out
+    m = torch.empty(rows, device=x.device, dtype=torch.float32) if return_stats else None
+    l = torch.empty(rows, device=x.device, dtype=torch.float32) if return_stats else None
+    check(lib.attn_softmax_rows(rows, cols, _DT[x.dtype], x.data_ptr(), x.stride(0),
+                                None if y is None else y.data_ptr(), 0 if y is None else y.stride(0),
+                                None if m is None else m.data_ptr(), None if l is None else l.data_ptr(),
+                                _stream(stream)), "attn_softmax_rows")
+    if return_stats:
+        return y, m, l
+    return y

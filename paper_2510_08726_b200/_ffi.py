@@ -22,7 +22,7 @@ ATTN_Q_POS_DEFAULT = -(1 << 63)
 
 EXPORTED = ("attn_fused_fwd", "attn_splitkv_default_splits", "attn_splitkv_workspace_bytes",
             "attn_splitkv_decode", "attn_combine", "attn_status_string", "attn_last_error",
-            "attn_abi_version", "attn_last_launch_count", "attn_merge_partials")
+            "attn_abi_version", "attn_last_launch_count", "attn_merge_partials", "attn_softmax_rows")
 
 
 class AttnTensor(ctypes.Structure):
@@ -74,6 +74,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.attn_merge_partials.argtypes = [i32, i64, i32, ctypes.c_int, vp, i64, i64, vp, i64, ctypes.c_int, vp, i64, vp,
                                         vp]
     lib.attn_merge_partials.restype = ctypes.c_int
+    lib.attn_softmax_rows.argtypes = [i64, i32, ctypes.c_int, vp, i64, vp, i64, vp, vp, vp]
+    lib.attn_softmax_rows.restype = ctypes.c_int
     lib.attn_status_string.argtypes = [ctypes.c_int]
     lib.attn_status_string.restype = ctypes.c_char_p
     lib.attn_last_error.restype = ctypes.c_char_p

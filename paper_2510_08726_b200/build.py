@@ -25,7 +25,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", 
 
 LIBS = {
     os.path.join(PKG, "libattn.so"): {
-        "sources": [os.path.join(CSRC, f) for f in ("api.cu", "fwd_tc.cu", "fwd_simt.cu", "decode.cu")],
+        "sources": [os.path.join(CSRC, f) for f in ("api.cu", "fwd_tc.cu", "fwd_simt.cu", "decode.cu", "softmax_rows.cu")],
         "headers": [os.path.join(CSRC, f) for f in ("ptx.cuh", "kernels.h")] + [os.path.join(ROOT, "include", "attn.h")],
     },
     os.path.join(ROOT, "datagen", "libdatagen.so"): {

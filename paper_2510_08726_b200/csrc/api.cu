@@ -367,4 +367,25 @@ attn_status attn_merge_partials(int32_t num_parts, int64_t rows, int32_t head_di
   return st;
 }
 
+attn_status attn_softmax_rows(int64_t rows, int32_t cols, attn_dtype dtype, const void* x, int64_t x_stride_row,
+                              void* y, int64_t y_stride_row, float* row_max, float* row_sum, attn_stream_t stream) {
+  g_err[0] = 0;
+  CHECK_ARG(rows >= 1 && cols >= 1, "extents must be >= 1");
+  CHECK_ARG(rows < (1LL << 31), "too many rows");
+  CHECK_ARG(dtype == ATTN_BF16 || dtype == ATTN_FP32 || dtype == ATTN_FP16, "unknown dtype");
+  CHECK_ARG(x != nullptr, "x is NULL");
+  CHECK_ARG(y != nullptr || row_max != nullptr || row_sum != nullptr, "no output requested");
+  const int eb = dtype == ATTN_FP32 ? 4 : 2;
+  CHECK_ARG(x_stride_row >= cols && (y == nullptr || y_stride_row >= cols), "row stride smaller than cols");
+  if ((reinterpret_cast<uintptr_t>(x) & 15) || ((x_stride_row * eb) & 15) ||
+      (y != nullptr && ((reinterpret_cast<uintptr_t>(y) & 15) || ((y_stride_row * eb) & 15))))
+    return fail(ATTN_ERR_ALIGNMENT, "x / y must be 16-byte aligned with 16-byte-multiple row strides");
+  attn::SoftmaxRowsArgs s{rows, cols, (int)dtype, x, x_stride_row, y, y_stride_row, row_max, row_sum};
+  int launches = 0;
+  attn_status st = cuda_status(attn::launch_softmax_rows(s, reinterpret_cast<cudaStream_t>(stream), &launches),
+                               "softmax_rows launch");
+  if (st == ATTN_OK) g_launches = launches;
+  return st;
+}
+
 }  // extern "C"

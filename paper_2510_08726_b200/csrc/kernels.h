@@ -88,4 +88,16 @@ struct MergeArgs {
 };
 cudaError_t launch_merge(const MergeArgs& a, cudaStream_t stream, int* launches);
 
+// ------------------------------------------------------------ NEXT-4: softmax rows (Fig. 2 chain)
+struct SoftmaxRowsArgs {
+  long long rows;
+  int cols;
+  int dtype;                    // attn_dtype value
+  const void* x; long long x_stride;
+  void* y; long long y_stride;  // nullable
+  float* row_max;               // nullable
+  float* row_sum;               // nullable
+};
+cudaError_t launch_softmax_rows(const SoftmaxRowsArgs& a, cudaStream_t stream, int* launches);
+
 }  // namespace attn

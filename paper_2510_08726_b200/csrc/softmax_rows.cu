@@ -1,0 +1,186 @@
+// softmax_rows.cu -- NEXT-4: the paper's motivating reduction chain (Fig. 2,
+// P:164-215) as a second workload: per row, xmax = max_j x, xsum =
+// sum_j exp(x - xmax) (Fig. 2a's result) and the normalised softmax
+// y = exp(x - xmax) / xsum, in ONE pass over HBM.
+//
+// Both of the paper's repairs appear: each thread reduces its register-resident
+// elements locally (privatisation, Fig. 19) and rolls its (m, l)
+// across row chunks with h(t, r, r') = exp(r - r') t (Rolling Update, Fig. 2c,
+// P:205-215); the 256 threads of the row then merge their partial (m, l) with
+// the Split-K global repair (Eq. 8).  Rows that fit in registers
+// (<= 8192 16-bit or 4096 fp32 elements) are read once and y is written from
+// registers; longer rows are re-read (from L2) for y.  HBM-bound: one read of
+// x and one write of y.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <math.h>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace attn {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kVecPerThread = 4;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+// 16-byte vector of T as floats
+template <typename T> struct Vec;
+template <> struct Vec<float> {
+  static constexpr int N = 4;
+  static __device__ __forceinline__ void load(const float* p, float (&f)[4]) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+    f[0] = v.x; f[1] = v.y; f[2] = v.z; f[3] = v.w;
+  }
+  static __device__ __forceinline__ void store(float* p, const float (&f)[4]) {
+    *reinterpret_cast<float4*>(p) = make_float4(f[0], f[1], f[2], f[3]);
+  }
+  static __device__ __forceinline__ float one(const float* p) { return __ldg(p); }
+  static __device__ __forceinline__ void put(float* p, float x) { *p = x; }
+};
+template <typename H, bool kBf16> struct Vec16 {
+  static constexpr int N = 8;
+  static __device__ __forceinline__ float cvt(uint16_t u) {
+    if constexpr (kBf16) return __uint_as_float((uint32_t)u << 16);
+    else return __half2float(__ushort_as_half(u));
+  }
+  static __device__ __forceinline__ uint16_t back(float x) {
+    if constexpr (kBf16) return __bfloat16_as_ushort(__float2bfloat16_rn(x));
+    else return __half_as_ushort(__float2half_rn(x));
+  }
+  static __device__ __forceinline__ void load(const H* p, float (&f)[8]) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      f[2 * i] = cvt((uint16_t)(w[i] & 0xFFFF));
+      f[2 * i + 1] = cvt((uint16_t)(w[i] >> 16));
+    }
+  }
+  static __device__ __forceinline__ void store(H* p, const float (&f)[8]) {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) w[i] = (uint32_t)back(f[2 * i]) | ((uint32_t)back(f[2 * i + 1]) << 16);
+    *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  static __device__ __forceinline__ float one(const H* p) { return cvt(*reinterpret_cast<const uint16_t*>(p)); }
+  static __device__ __forceinline__ void put(H* p, float x) { *reinterpret_cast<uint16_t*>(p) = back(x); }
+};
+template <> struct Vec<__nv_bfloat16> : Vec16<__nv_bfloat16, true> {};
+template <> struct Vec<__half> : Vec16<__half, false> {};
+
+// Eq. 8 merge of two (m, l) partials in log2 units: the repair term
+// exp2(m_i - M) tag-updates each partial sum to the common reference M.
+__device__ __forceinline__ void merge_ml(float& m, float& l, float m2, float l2) {
+  const float M = fmaxf(m, m2);
+  if (M == -INFINITY) return;                    // both empty
+  l = (m == -INFINITY ? 0.f : l * ex2_approx(m - M)) + (m2 == -INFINITY ? 0.f : l2 * ex2_approx(m2 - M));
+  m = M;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) softmax_rows_kernel(const SoftmaxRowsArgs a) {
+  using V = Vec<T>;
+  constexpr int E = V::N * kVecPerThread;                   // elements per thread per chunk
+  constexpr int kChunk = E * kThreads;                      // elements per chunk
+  const long long row = blockIdx.x;
+  const T* x = static_cast<const T*>(a.x) + row * a.x_stride;
+  T* y = a.y ? static_cast<T*>(a.y) + row * a.y_stride : nullptr;
+  const int tid = threadIdx.x;
+
+  float v[E];
+  auto load_chunk = [&](int c0) {                           // x * log2(e), -inf outside the row
+#pragma unroll
+    for (int q = 0; q < kVecPerThread; ++q) {
+      const int col = c0 + (q * kThreads + tid) * V::N;
+      float f[V::N];
+      if (col + V::N <= a.cols) {
+        V::load(x + col, f);
+      } else {
+#pragma unroll
+        for (int e = 0; e < V::N; ++e) f[e] = col + e < a.cols ? V::one(x + col + e) : -INFINITY;
+      }
+#pragma unroll
+      for (int e = 0; e < V::N; ++e) v[q * V::N + e] = f[e] * kLog2e;
+    }
+  };
+
+  // ---- local (privatised) reductions, rolled across chunks (Fig. 2c repair)
+  float m = -INFINITY, l = 0.f;
+  const int nchunk = (a.cols + kChunk - 1) / kChunk;
+  for (int ch = 0; ch < nchunk; ++ch) {
+    load_chunk(ch * kChunk);
+    float mx = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < E; ++e) mx = fmaxf(mx, v[e]);        // max_local
+    if (mx != -INFINITY) {
+      float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+      for (int e = 0; e < E; e += 2) {                       // sum_local
+        s0 += ex2_approx(v[e] - mx);
+        s1 += ex2_approx(v[e + 1] - mx);
+      }
+      merge_ml(m, l, mx, s0 + s1);                           // xsum = h(xsum) + xsump
+    }
+  }
+  // ---- global section across the row's threads (Eq. 8)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o), l2 = __shfl_xor_sync(0xffffffffu, l, o);
+    merge_ml(m, l, m2, l2);
+  }
+  __shared__ float sm[kThreads / 32], sl[kThreads / 32];
+  if ((tid & 31) == 0) {
+    sm[tid >> 5] = m;
+    sl[tid >> 5] = l;
+  }
+  __syncthreads();
+  float M = -INFINITY, L = 0.f;
+#pragma unroll
+  for (int w = 0; w < kThreads / 32; ++w) merge_ml(M, L, sm[w], sl[w]);
+
+  if (tid == 0) {
+    if (a.row_max) a.row_max[row] = M == -INFINITY ? -INFINITY : M * kLn2;
+    if (a.row_sum) a.row_sum[row] = L;
+  }
+  if (y == nullptr) return;
+  // ---- y = exp(x - M) / L  (from registers when the row is one chunk)
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  const float Mu = M == -INFINITY ? 0.f : M;
+  for (int ch = 0; ch < nchunk; ++ch) {
+    if (nchunk > 1) load_chunk(ch * kChunk);
+#pragma unroll
+    for (int q = 0; q < kVecPerThread; ++q) {
+      const int col = ch * kChunk + (q * kThreads + tid) * V::N;
+      float f[V::N];
+#pragma unroll
+      for (int e = 0; e < V::N; ++e) f[e] = ex2_approx(v[q * V::N + e] - Mu) * inv;
+      if (col + V::N <= a.cols) {
+        V::store(y + col, f);
+      } else {
+#pragma unroll
+        for (int e = 0; e < V::N; ++e)
+          if (col + e < a.cols) V::put(y + col + e, f[e]);
+      }
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_softmax_rows(const SoftmaxRowsArgs& a, cudaStream_t stream, int* launches) {
+  const unsigned grid = (unsigned)a.rows;
+  if (a.dtype == 1)
+    softmax_rows_kernel<float><<<grid, kThreads, 0, stream>>>(a);
+  else if (a.dtype == 2)
+    softmax_rows_kernel<__half><<<grid, kThreads, 0, stream>>>(a);
+  else
+    softmax_rows_kernel<__nv_bfloat16><<<grid, kThreads, 0, stream>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && launches) ++*launches;
+  return e;
+}
+
+}  // namespace attn

@@ -158,3 +158,25 @@ def test_R8_lazy_rescale_equals_definition(tau):
         o, l = oracle.rolling_update_lazy_bh(p, q, k, v, 1, b, tau)
         np.testing.assert_allclose(o, ref_o, rtol=1e-11, atol=1e-12)
         np.testing.assert_allclose(l, ref_l, rtol=1e-12, atol=1e-12)
+
+
+def test_softmax_rows_pins(golden):
+    """oracle.softmax_rows (vectorised Fig. 2a) against the Fig. 2 golden values, the
+    loop-for-loop Fig. 2a/2c programs, scipy's logsumexp and softmax invariants."""
+    from scipy.special import logsumexp
+    c = golden["FIG2_softmax_denominator"]
+    m, l, y = oracle.softmax_rows(np.array(c["inp"]))
+    np.testing.assert_allclose(l, c["xsum"], atol=1e-15)
+    np.testing.assert_array_equal(m, [3.0, 3.0])
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal((6, 37)) * 5
+    x[2, 1::3] = -np.inf
+    m, l, y = oracle.softmax_rows(x)
+    np.testing.assert_allclose(l, oracle.softmax_denominator(x), rtol=1e-13)
+    np.testing.assert_allclose(l, oracle.softmax_denominator_rolling(x), rtol=1e-12)
+    np.testing.assert_allclose(m + np.log(l), logsumexp(x, axis=1), rtol=1e-13)
+    np.testing.assert_allclose(y.sum(axis=1), 1.0, atol=1e-13)
+    np.testing.assert_allclose(oracle.softmax_rows(x + 7.25)[2], y, atol=1e-15)   # shift invariance
+    z = np.full((2, 5), -np.inf)
+    zm, zl, zy = oracle.softmax_rows(z)
+    assert np.all(zm == -np.inf) and np.all(zl == 0) and np.all(zy == 0)

@@ -6,7 +6,7 @@ OUT=gpurun_out/iter_$TAG.log
 : > $OUT
 timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "${PYTEST_K:-prefill or fp32}" --timeout 300 -p no:cacheprovider 2>&1 | tail -15 >> $OUT
 for w in ${WORKLOADS:-mha mha_causal gqa_window var_scaled_dot var_alibi_causal var_softcap_causal}; do
-  timeout 300 python bench.py --steps 20 --warmup 5 --no-e2e --no-decode --no-cpu --workload $w 2>&1 | \
+  timeout 300 python bench.py --steps 20 --warmup 5 --no-e2e --no-decode --no-cpu --no-softmax --workload $w 2>&1 | \
     python -c "import sys,json
 for l in sys.stdin:
     try: d=json.loads(l)

@@ -4,7 +4,7 @@ cd "$GRAFT_REPO_ROOT"
 OUT=gpurun_out/variants_${1:-x}.log; : > $OUT
 for lib in build/var_*/libattn.so; do
   for w in ${WORKLOADS:-mha mha_causal}; do
-    ATTN_LIB_PATH=$PWD/$lib timeout 300 python bench.py --steps 20 --warmup 5 --no-e2e --no-decode --no-cpu --workload $w 2>&1 | \
+    ATTN_LIB_PATH=$PWD/$lib timeout 300 python bench.py --steps 20 --warmup 5 --no-e2e --no-decode --no-cpu --no-softmax --workload $w 2>&1 | \
       python -c "import sys,json
 for l in sys.stdin:
     try: d=json.loads(l)

@@ -5,7 +5,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 lib_path = os.path.join(ROOT, "build", "libattn_trace.so")
 if not os.path.exists(lib_path):
-    src = [os.path.join(ROOT, "paper_2510_08726_b200", "csrc", f) for f in ("api.cu", "fwd_tc.cu", "fwd_simt.cu", "decode.cu")]
+    src = [os.path.join(ROOT, "paper_2510_08726_b200", "csrc", f) for f in ("api.cu", "fwd_tc.cu", "fwd_simt.cu", "decode.cu", "softmax_rows.cu")]
     subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
                            "-Xcompiler", "-fPIC", "-DATTN_TRACE", "-shared", "-o", lib_path] + os.environ.get("NVCC_EXTRA", "").split() + src)
 import torch
