@@ -6,7 +6,7 @@
 // Both of the paper's repairs appear: each thread reduces its register-resident
 // elements locally (privatisation, Fig. 19) and rolls its (m, l)
 // across row chunks with h(t, r, r') = exp(r - r') t (Rolling Update, Fig. 2c,
-// P:205-215); the 256 threads of the row then merge their partial (m, l) with
+// P:205-215); the row's 32-256 threads then merge their partial (m, l) with
 // the Split-K global repair (Eq. 8).  Rows that fit in registers
 // (<= 8192 16-bit or 4096 fp32 elements) are read once and y is written from
 // registers; longer rows are re-read (from L2) for y.  HBM-bound: one read of
@@ -21,7 +21,6 @@
 namespace attn {
 namespace {
 
-constexpr int kThreads = 256;
 constexpr int kVecPerThread = 4;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
@@ -80,11 +79,11 @@ __device__ __forceinline__ void merge_ml(float& m, float& l, float m2, float l2)
   m = M;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kThreads) softmax_rows_kernel(const SoftmaxRowsArgs a) {
+template <typename T, int kT>
+__global__ void __launch_bounds__(kT) softmax_rows_kernel(const SoftmaxRowsArgs a) {
   using V = Vec<T>;
   constexpr int E = V::N * kVecPerThread;                   // elements per thread per chunk
-  constexpr int kChunk = E * kThreads;                      // elements per chunk
+  constexpr int kChunk = E * kT;                            // elements per chunk
   const long long row = blockIdx.x;
   const T* x = static_cast<const T*>(a.x) + row * a.x_stride;
   T* y = a.y ? static_cast<T*>(a.y) + row * a.y_stride : nullptr;
@@ -94,7 +93,7 @@ __global__ void __launch_bounds__(kThreads) softmax_rows_kernel(const SoftmaxRow
   auto load_chunk = [&](int c0) {                           // x * log2(e), -inf outside the row
 #pragma unroll
     for (int q = 0; q < kVecPerThread; ++q) {
-      const int col = c0 + (q * kThreads + tid) * V::N;
+      const int col = c0 + (q * kT + tid) * V::N;
       float f[V::N];
       if (col + V::N <= a.cols) {
         V::load(x + col, f);
@@ -107,56 +106,74 @@ __global__ void __launch_bounds__(kThreads) softmax_rows_kernel(const SoftmaxRow
     }
   };
 
-  // ---- local (privatised) reductions, rolled across chunks (Fig. 2c repair)
-  float m = -INFINITY, l = 0.f;
+  // ---- local (privatised) reductions, rolled across chunks (Fig. 2c repair).
+  // v[] keeps exp2(x - mx) of the last chunk so a one-chunk row needs no
+  // second exponential for y.
+  float m = -INFINITY, l = 0.f, mx = -INFINITY;
   const int nchunk = (a.cols + kChunk - 1) / kChunk;
   for (int ch = 0; ch < nchunk; ++ch) {
     load_chunk(ch * kChunk);
-    float mx = -INFINITY;
+    mx = -INFINITY;
 #pragma unroll
     for (int e = 0; e < E; ++e) mx = fmaxf(mx, v[e]);        // max_local
     if (mx != -INFINITY) {
       float s0 = 0.f, s1 = 0.f;
 #pragma unroll
       for (int e = 0; e < E; e += 2) {                       // sum_local
-        s0 += ex2_approx(v[e] - mx);
-        s1 += ex2_approx(v[e + 1] - mx);
+        v[e] = ex2_approx(v[e] - mx);
+        v[e + 1] = ex2_approx(v[e + 1] - mx);
+        s0 += v[e];
+        s1 += v[e + 1];
       }
       merge_ml(m, l, mx, s0 + s1);                           // xsum = h(xsum) + xsump
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[e] = 0.f;
     }
   }
   // ---- global section across the row's threads (Eq. 8)
+  float M = m, L = l;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    const float m2 = __shfl_xor_sync(0xffffffffu, m, o), l2 = __shfl_xor_sync(0xffffffffu, l, o);
-    merge_ml(m, l, m2, l2);
+    const float m2 = __shfl_xor_sync(0xffffffffu, M, o), l2 = __shfl_xor_sync(0xffffffffu, L, o);
+    merge_ml(M, L, m2, l2);
   }
-  __shared__ float sm[kThreads / 32], sl[kThreads / 32];
-  if ((tid & 31) == 0) {
-    sm[tid >> 5] = m;
-    sl[tid >> 5] = l;
-  }
-  __syncthreads();
-  float M = -INFINITY, L = 0.f;
+  if constexpr (kT > 32) {
+    __shared__ float sm[kT / 32], sl[kT / 32];
+    if ((tid & 31) == 0) {
+      sm[tid >> 5] = M;
+      sl[tid >> 5] = L;
+    }
+    __syncthreads();
+    M = -INFINITY;
+    L = 0.f;
 #pragma unroll
-  for (int w = 0; w < kThreads / 32; ++w) merge_ml(M, L, sm[w], sl[w]);
-
+    for (int w = 0; w < kT / 32; ++w) merge_ml(M, L, sm[w], sl[w]);
+  }
   if (tid == 0) {
     if (a.row_max) a.row_max[row] = M == -INFINITY ? -INFINITY : M * kLn2;
     if (a.row_sum) a.row_sum[row] = L;
   }
   if (y == nullptr) return;
-  // ---- y = exp(x - M) / L  (from registers when the row is one chunk)
+  // ---- y = exp(x - M) / L
   const float inv = L > 0.f ? 1.f / L : 0.f;
   const float Mu = M == -INFINITY ? 0.f : M;
   for (int ch = 0; ch < nchunk; ++ch) {
-    if (nchunk > 1) load_chunk(ch * kChunk);
+    float scale;
+    if (nchunk > 1) {
+      load_chunk(ch * kChunk);
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[e] = ex2_approx(v[e] - Mu);
+      scale = inv;
+    } else {
+      scale = mx == -INFINITY ? 0.f : ex2_approx(mx - Mu) * inv;   // tag-update exp2(x - mx) to M
+    }
 #pragma unroll
     for (int q = 0; q < kVecPerThread; ++q) {
-      const int col = ch * kChunk + (q * kThreads + tid) * V::N;
+      const int col = ch * kChunk + (q * kT + tid) * V::N;
       float f[V::N];
 #pragma unroll
-      for (int e = 0; e < V::N; ++e) f[e] = ex2_approx(v[q * V::N + e] - Mu) * inv;
+      for (int e = 0; e < V::N; ++e) f[e] = v[q * V::N + e] * scale;
       if (col + V::N <= a.cols) {
         V::store(y + col, f);
       } else {
@@ -168,17 +185,25 @@ __global__ void __launch_bounds__(kThreads) softmax_rows_kernel(const SoftmaxRow
   }
 }
 
+template <typename T>
+cudaError_t launch_rows_t(const SoftmaxRowsArgs& a, cudaStream_t stream) {
+  // threads per row: enough for the row to be one chunk of kVecPerThread vectors per thread
+  const int per_thread = Vec<T>::N * kVecPerThread;
+  const int need = (a.cols + per_thread - 1) / per_thread;
+  const unsigned grid = (unsigned)a.rows;
+  if (need <= 32) softmax_rows_kernel<T, 32><<<grid, 32, 0, stream>>>(a);
+  else if (need <= 64) softmax_rows_kernel<T, 64><<<grid, 64, 0, stream>>>(a);
+  else if (need <= 128) softmax_rows_kernel<T, 128><<<grid, 128, 0, stream>>>(a);
+  else softmax_rows_kernel<T, 256><<<grid, 256, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 cudaError_t launch_softmax_rows(const SoftmaxRowsArgs& a, cudaStream_t stream, int* launches) {
-  const unsigned grid = (unsigned)a.rows;
-  if (a.dtype == 1)
-    softmax_rows_kernel<float><<<grid, kThreads, 0, stream>>>(a);
-  else if (a.dtype == 2)
-    softmax_rows_kernel<__half><<<grid, kThreads, 0, stream>>>(a);
-  else
-    softmax_rows_kernel<__nv_bfloat16><<<grid, kThreads, 0, stream>>>(a);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = a.dtype == 1 ? launch_rows_t<float>(a, stream)
+                               : (a.dtype == 2 ? launch_rows_t<__half>(a, stream)
+                                               : launch_rows_t<__nv_bfloat16>(a, stream));
   if (e == cudaSuccess && launches) ++*launches;
   return e;
 }
