@@ -526,6 +526,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tmem_st_wait();
       l += sum;
+#ifdef ATTN_STRICT_WAITS
+      // Sanitizer build: observe every o_done phase (the production kernel only
+      // waits when it rescales O; it can never fall two phases behind).
+      if (it > 0 && !__any_sync(0xffffffffu, need_o)) {
+        mbar_wait(&o_done[t], (it - 1) & 1);
+        tc_fence_after();
+      }
+#endif
       tc_fence_before();
       if (t == 0 && lane == 0 && wt < 4) TRACE(20 + wq, j);
       named_bar_arrive(kBarP0 + t, kTileThreads + 32);   // P_t(j) in TMEM -> MMA issuer
