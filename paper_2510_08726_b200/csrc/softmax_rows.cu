@@ -185,6 +185,179 @@ __global__ void __launch_bounds__(kT) softmax_rows_kernel(const SoftmaxRowsArgs 
   }
 }
 
+// 16-bit inputs: the chunk stays in registers as the raw 16-byte vectors
+// (16 registers for 32 elements); the row max is taken on packed pairs and the
+// exp2 values overwrite the raw words as f16 pairs (values in (0, 1], 11-bit
+// significand, below the bf16 output rounding), so the kernel needs half the
+// registers of the float copy and twice the resident rows per SM (the HBM
+// stream needs bytes in flight, Little's law).
+template <bool kBf16> struct Raw16;
+template <> struct Raw16<true> {
+  static constexpr uint16_t kNegInf = 0xFF80u;
+  static __device__ __forceinline__ uint32_t hmax2(uint32_t a, uint32_t b) {
+    __nv_bfloat162 r = __hmax2(*reinterpret_cast<__nv_bfloat162*>(&a), *reinterpret_cast<__nv_bfloat162*>(&b));
+    return *reinterpret_cast<uint32_t*>(&r);
+  }
+  static __device__ __forceinline__ float lo(uint32_t w) { return __uint_as_float(w << 16); }
+  static __device__ __forceinline__ float hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+  static __device__ __forceinline__ uint32_t back2(float x0, float x1) {
+    __nv_bfloat162 r = __floats2bfloat162_rn(x0, x1);
+    return *reinterpret_cast<uint32_t*>(&r);
+  }
+};
+template <> struct Raw16<false> {
+  static constexpr uint16_t kNegInf = 0xFC00u;
+  static __device__ __forceinline__ uint32_t hmax2(uint32_t a, uint32_t b) {
+    __half2 r = __hmax2(*reinterpret_cast<__half2*>(&a), *reinterpret_cast<__half2*>(&b));
+    return *reinterpret_cast<uint32_t*>(&r);
+  }
+  static __device__ __forceinline__ float lo(uint32_t w) { return __half2float(__ushort_as_half((uint16_t)(w & 0xFFFF))); }
+  static __device__ __forceinline__ float hi(uint32_t w) { return __half2float(__ushort_as_half((uint16_t)(w >> 16))); }
+  static __device__ __forceinline__ uint32_t back2(float x0, float x1) {
+    __half2 r = __floats2half2_rn(x0, x1);
+    return *reinterpret_cast<uint32_t*>(&r);
+  }
+};
+__device__ __forceinline__ float f16lo(uint32_t w) { return __half2float(__ushort_as_half((uint16_t)(w & 0xFFFF))); }
+__device__ __forceinline__ float f16hi(uint32_t w) { return __half2float(__ushort_as_half((uint16_t)(w >> 16))); }
+
+#ifndef SMR_MINB
+#define SMR_MINB 1536   // resident threads per SM to fit (caps registers at 40: 12 x 128-thread rows)
+#endif
+template <bool kBf16, int kT>
+__global__ void __launch_bounds__(kT, SMR_MINB ? SMR_MINB / kT : 1) softmax_rows16_kernel(const SoftmaxRowsArgs a) {
+  using R = Raw16<kBf16>;
+  constexpr int kChunk = 8 * kVecPerThread * kT;
+  const long long row = blockIdx.x;
+  const uint16_t* x = static_cast<const uint16_t*>(a.x) + row * a.x_stride;
+  uint16_t* y = a.y ? static_cast<uint16_t*>(a.y) + row * a.y_stride : nullptr;
+  const int tid = threadIdx.x;
+
+  uint32_t r[kVecPerThread][4];
+  auto load_chunk = [&](int c0) {
+#pragma unroll
+    for (int q = 0; q < kVecPerThread; ++q) {
+      const int col = c0 + (q * kT + tid) * 8;
+      if (col + 8 <= a.cols) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(x + col));
+        r[q][0] = v.x; r[q][1] = v.y; r[q][2] = v.z; r[q][3] = v.w;
+      } else {
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const uint32_t l0 = col + 2 * w < a.cols ? x[col + 2 * w] : R::kNegInf;
+          const uint32_t h0 = col + 2 * w + 1 < a.cols ? x[col + 2 * w + 1] : R::kNegInf;
+          r[q][w] = l0 | (h0 << 16);
+        }
+      }
+    }
+  };
+
+  float m = -INFINITY, l = 0.f, mx = -INFINITY;             // log2 units
+  const int nchunk = (a.cols + kChunk - 1) / kChunk;
+  for (int ch = 0; ch < nchunk; ++ch) {
+    load_chunk(ch * kChunk);
+    uint32_t pm = r[0][0];                                   // max_local on packed pairs
+#pragma unroll
+    for (int q = 0; q < kVecPerThread; ++q)
+#pragma unroll
+      for (int w = 0; w < 4; ++w) pm = R::hmax2(pm, r[q][w]);
+    mx = fmaxf(R::lo(pm), R::hi(pm)) * kLog2e;
+    if (mx != -INFINITY) {
+      float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+      for (int q = 0; q < kVecPerThread; ++q)
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {                        // sum_local
+          const float e0 = ex2_approx(fmaf(R::lo(r[q][w]), kLog2e, -mx));
+          const float e1 = ex2_approx(fmaf(R::hi(r[q][w]), kLog2e, -mx));
+          s0 += e0;
+          s1 += e1;
+          const __half2 h = __floats2half2_rn(e0, e1);
+          r[q][w] = *reinterpret_cast<const uint32_t*>(&h);
+        }
+      merge_ml(m, l, mx, s0 + s1);                           // xsum = h(xsum) + xsump
+    } else {
+#pragma unroll
+      for (int q = 0; q < kVecPerThread; ++q)
+#pragma unroll
+        for (int w = 0; w < 4; ++w) r[q][w] = 0u;
+    }
+  }
+  float M = m, L = l;                                        // global section (Eq. 8)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, M, o), l2 = __shfl_xor_sync(0xffffffffu, L, o);
+    merge_ml(M, L, m2, l2);
+  }
+  if constexpr (kT > 32) {
+    __shared__ float sm[kT / 32], sl[kT / 32];
+    if ((tid & 31) == 0) {
+      sm[tid >> 5] = M;
+      sl[tid >> 5] = L;
+    }
+    __syncthreads();
+    M = -INFINITY;
+    L = 0.f;
+#pragma unroll
+    for (int w = 0; w < kT / 32; ++w) merge_ml(M, L, sm[w], sl[w]);
+  }
+  if (tid == 0) {
+    if (a.row_max) a.row_max[row] = M == -INFINITY ? -INFINITY : M * kLn2;
+    if (a.row_sum) a.row_sum[row] = L;
+  }
+  if (y == nullptr) return;
+  const float inv = L > 0.f ? 1.f / L : 0.f;                 // y = exp(x - M) / L
+  const float Mu = M == -INFINITY ? 0.f : M;
+#ifndef SMR_REV
+#define SMR_REV 1
+#endif
+  for (int c = 0; c < nchunk; ++c) {
+    const int ch = SMR_REV ? nchunk - 1 - c : c;   // reverse: the re-read starts with the L2-hottest chunk
+    uint32_t o[kVecPerThread][4];
+    if (nchunk > 1) {
+      load_chunk(ch * kChunk);
+#pragma unroll
+      for (int q = 0; q < kVecPerThread; ++q)
+#pragma unroll
+        for (int w = 0; w < 4; ++w)
+          o[q][w] = R::back2(ex2_approx(fmaf(R::lo(r[q][w]), kLog2e, -Mu)) * inv,
+                             ex2_approx(fmaf(R::hi(r[q][w]), kLog2e, -Mu)) * inv);
+    } else {
+      const float scale = mx == -INFINITY ? 0.f : ex2_approx(mx - Mu) * inv;   // tag-update to M
+#pragma unroll
+      for (int q = 0; q < kVecPerThread; ++q)
+#pragma unroll
+        for (int w = 0; w < 4; ++w) o[q][w] = R::back2(f16lo(r[q][w]) * scale, f16hi(r[q][w]) * scale);
+    }
+#pragma unroll
+    for (int q = 0; q < kVecPerThread; ++q) {
+      const int col = ch * kChunk + (q * kT + tid) * 8;
+      if (col + 8 <= a.cols) {
+        *reinterpret_cast<uint4*>(y + col) = make_uint4(o[q][0], o[q][1], o[q][2], o[q][3]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if (col + e < a.cols) y[col + e] = (uint16_t)(o[q][e >> 1] >> (16 * (e & 1)));
+      }
+    }
+  }
+}
+
+#ifndef SMR_T512
+#define SMR_T512 0      // 1: rows of 8193..16384 16-bit elements as one 512-thread chunk (measured slower: 3 resident rows)
+#endif
+template <bool kBf16>
+cudaError_t launch_rows16(const SoftmaxRowsArgs& a, cudaStream_t stream) {
+  const int need = (a.cols + 8 * kVecPerThread - 1) / (8 * kVecPerThread);
+  const unsigned grid = (unsigned)a.rows;
+  if (need <= 32) softmax_rows16_kernel<kBf16, 32><<<grid, 32, 0, stream>>>(a);
+  else if (need <= 64) softmax_rows16_kernel<kBf16, 64><<<grid, 64, 0, stream>>>(a);
+  else if (need <= 128) softmax_rows16_kernel<kBf16, 128><<<grid, 128, 0, stream>>>(a);
+  else if (need <= 256 || !SMR_T512) softmax_rows16_kernel<kBf16, 256><<<grid, 256, 0, stream>>>(a);
+  else softmax_rows16_kernel<kBf16, 512><<<grid, 512, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t launch_rows_t(const SoftmaxRowsArgs& a, cudaStream_t stream) {
   // threads per row: enough for the row to be one chunk of kVecPerThread vectors per thread
@@ -201,9 +374,13 @@ cudaError_t launch_rows_t(const SoftmaxRowsArgs& a, cudaStream_t stream) {
 }  // namespace
 
 cudaError_t launch_softmax_rows(const SoftmaxRowsArgs& a, cudaStream_t stream, int* launches) {
-  cudaError_t e = a.dtype == 1 ? launch_rows_t<float>(a, stream)
-                               : (a.dtype == 2 ? launch_rows_t<__half>(a, stream)
-                                               : launch_rows_t<__nv_bfloat16>(a, stream));
+#ifndef SMR_FLOAT16
+#define SMR_FLOAT16 0   // 1: 16-bit rows through the float-register kernel (A/B)
+#endif
+  cudaError_t e;
+  if (a.dtype == 1) e = launch_rows_t<float>(a, stream);
+  else if (SMR_FLOAT16) e = a.dtype == 2 ? launch_rows_t<__half>(a, stream) : launch_rows_t<__nv_bfloat16>(a, stream);
+  else e = a.dtype == 2 ? launch_rows16<false>(a, stream) : launch_rows16<true>(a, stream);
   if (e == cudaSuccess && launches) ++*launches;
   return e;
 }
