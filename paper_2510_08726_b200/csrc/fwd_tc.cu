@@ -9,20 +9,23 @@
 // O / l after the loop (Fig. 9 reverse_compute_at(norm)).
 //
 // B200 mapping:
-//   CTA = 2 query tiles of BM = 128 rows of one (b, hq) -> 256 rows; 384 threads.
+//   CTA = 2 query tiles of BM = 128 rows of one (b, hq) -> 256 rows; 352 threads.
 //   warps 0-3   : softmax/correction/epilogue for query tile 0 (thread = row)
 //   warps 4-7   : same for query tile 1
-//   warp 8      : TMA producer (Q once; K_j / V_j through a ring of kStages slots,
-//                 plus L2 prefetch kPrefetch tiles ahead)
-//   warp 9      : tcgen05.mma issuer (one thread)
+//   warp 8      : TMA producer (Q once; K_j / V_j through a ring of kStages slots)
+//   warp 9      : tcgen05.mma issuer (warp-wide, one elected lane issues)
 //   warp 10     : TMEM allocator (512 columns)
 //   The producer and MMA warps get the HIGHEST warp ids on purpose: the warp
 //   arbiter is highest-id-first, so they are never starved by the softmax warps.
-//   TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512) (fp32 columns);
-//         P_t (bf16) overwrites the first 64 columns of S_t and feeds the
-//         PV MMA straight from TMEM (A operand in TMEM).
-//   MMA issue order per KV step j: PV0(j), QK0(j+1), PV1(j), QK1(j+1), so the
-//   tensor core runs one tile's MMAs while the other tile's softmax runs.
+//   TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512) (fp32 columns).
+//   P_t (bf16/fp16) goes to shared memory in the UMMA K-major layout (default,
+//   ATTN_P_SMEM=1): S_t is free as soon as its softmax threads hold it in
+//   registers, so the issue order per KV step j is PV0(j), QK0(j+2), PV1(j),
+//   QK1(j+2) and S_t(j+1) is computed while the softmax of step j runs; K
+//   runs two tiles ahead of V in the 3-slot ring.  (ATTN_P_SMEM=0: P aliases
+//   the first 64 columns of S_t in TMEM and feeds a TS MMA; order PV0(j),
+//   QK0(j+1), PV1(j), QK1(j+1) -- the tile's chain softmax -> PV -> QK is
+//   serial; measured 3 % slower.)
 //   Repair is lazy (reading R9): the reference max r' only moves when the
 //   running max exceeds it by more than kTau (log2 units); exact because h
 //   tag-updates to any reference (Eq. 6).
@@ -59,9 +62,19 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr uint32_t kBarTok0 = 3, kBarTok1 = 4;   // named barriers of the exp token
 constexpr uint32_t kBarP0 = 5;                    // 5 / 6: "P_t ready" (softmax threads of tile t + MMA warp)
 constexpr uint32_t kBarX0 = 7;                    // 7 / 8: row-max / row-sum exchange between column halves
+constexpr uint32_t kBarS0 = 9;                    // 9 / 10: "S_t loaded into registers" (P in smem only)
 #ifndef ATTN_TOKEN
 #define ATTN_TOKEN 1
 #endif
+#ifndef ATTN_P_SMEM
+#define ATTN_P_SMEM 1
+#endif
+// P in shared memory (PV = SS MMA) instead of aliasing S in TMEM: S_t is free
+// as soon as the softmax threads have loaded it, so QK_t(j+2) is issued right
+// after PV_t(j) and overlaps the softmax of step j+1 (the TMEM-aliased P
+// serialises softmax -> PV -> QK -> softmax per tile).  Costs 64 KiB of
+// shared memory (the K/V ring shrinks to 3 stages at D = 128).
+constexpr bool kPSmem = ATTN_P_SMEM != 0;
 constexpr bool kToken = ATTN_TOKEN != 0;   // alternate the two softmax warpgroups' exp phases
 
 #ifdef ATTN_SOFTMAX_SPIN
@@ -74,17 +87,24 @@ constexpr bool kToken = ATTN_TOKEN != 0;   // alternate the two softmax warpgrou
 #else
 #define WAIT_LM(bar, par) mbar_wait(bar, par)
 #endif
+#ifndef ATTN_LOADER_SLEEP
+#define ATTN_LOADER_SLEEP 0
+#endif
+// The producer's ring-slot waits: try_wait (the thread sleeps in hardware, no
+// issue slots taken from the softmax warp on its SM sub-partition) or poll.
+#define WAIT_L(bar, par) do { if (ATTN_LOADER_SLEEP) mbar_wait(bar, par); else WAIT_LM(bar, par); } while (0)
 
 #ifdef ATTN_TRACE
 // Debug-only timeline of one CTA: clock64() per (event, step), kept in shared
 // memory while the kernel runs (so tracing adds no global-memory traffic
 // before the mbarrier releases) and copied to g_trace at the end.
-constexpr int kTrEv = 26, kTrSteps = 40;
-__device__ long long g_trace[kTrEv][kTrSteps];
+// 32-bit clock() samples (the host unwraps differences modulo 2^32).
+constexpr int kTrEv = 26, kTrSteps = kPSmem ? 24 : 40;
+__device__ long long g_trace[kTrEv][40];
 __device__ __forceinline__ bool trace_cta() { return blockIdx.x == 5 && blockIdx.y == 3 && blockIdx.z == 2; }
 #define TRACE(ev, step)                                                          \
   do {                                                                           \
-    if (trace_cta() && (step) < kTrSteps) s_trace[(ev) * kTrSteps + (step)] = clock64(); \
+    if (trace_cta() && (step) < kTrSteps) s_trace[(ev) * kTrSteps + (step)] = (uint32_t)clock(); \
   } while (0)
 #else
 #define TRACE(ev, step) do { } while (0)
@@ -95,20 +115,24 @@ struct Cfg {
   static constexpr int kBoxes = D / 64;           // 64-column (128 B) swizzle atoms per row
   static constexpr int kQTileBytes = BM * D * 2;
   static constexpr int kKVTileBytes = BN * D * 2;
+  // P in shared memory at D = 128 only: at D = 64 the tile's MMAs are half as long, the
+  // exponentials dominate and the P stores cost more than the decoupling gains (measured).
+  static constexpr bool kPS = kPSmem && D == 128;
+  static constexpr int kPTileBytes = kPS ? BM * BN * 2 : 0;
 #ifdef ATTN_TRACE
-  static constexpr int kStages = (D == 128) ? 4 : 8;   // room for the shared-memory trace
+  static constexpr int kStages = kPS ? 3 : ((D == 128) ? 4 : 8);   // room for the trace
 #else
-  static constexpr int kStages = (D == 128) ? 5 : 10;
+  static constexpr int kStages = kPS ? 3 : ((D == 128) ? 5 : 10);
 #endif
   // Load-group barriers (ring).  The producer can be at most kStages/2 groups
   // ahead of the issuer's wait, so kStages/2 + 1 barriers never alias a phase.
   static constexpr int kPairBars = kStages / 2 + 1;
-  static constexpr int kSmemQ = 2 * kQTileBytes;
+  static constexpr int kSmemQ = 2 * kQTileBytes + 2 * kPTileBytes;   // Q tiles, then P tiles
   static constexpr int kSmemKV = kStages * kKVTileBytes;
   static constexpr int kNumBars = 1 + 2 * kStages + 6;
   static constexpr int kXchgBytes = kHalves > 1 ? 2 * kHalves * BM * 4 : 0;   // [tile][half][row] floats
 #ifdef ATTN_TRACE
-  static constexpr int kSmemBytes = kSmemQ + kSmemKV + kXchgBytes + 1024 + 26 * 40 * 8;
+  static constexpr int kSmemBytes = kSmemQ + kSmemKV + kXchgBytes + 256 + kTrEv * kTrSteps * 4;
 #else
   static constexpr int kSmemBytes = kSmemQ + kSmemKV + kXchgBytes + kNumBars * 8 + 16;
 #endif
@@ -213,6 +237,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o, const Shape s,
                   const VariantParams v, float* __restrict__ lse) {
   using C = Cfg<D>;
+  constexpr bool kPSmem = C::kPS;   // shadows the global switch: per head dim
   constexpr bool kPlain = !kAlibi && !kSoftcap;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // The 128-byte swizzle needs 1024-byte aligned tiles; dynamic shared memory
@@ -220,6 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if ((smem_u32(smem_raw) & 1023) != 0) __trap();
   uint8_t* smem = smem_raw;
   uint8_t* sQ = smem;
+  uint8_t* sP = smem + 2 * C::kQTileBytes;   // kPSmem: P_t, K-major SW128 [key atom][row][128 B]
   uint8_t* sKV = smem + C::kSmemQ;
   float* xchg = reinterpret_cast<float*>(sKV + C::kSmemKV);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::kSmemKV + C::kXchgBytes);
@@ -231,7 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* o_done = p_ready + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 #ifdef ATTN_TRACE
-  long long* s_trace = reinterpret_cast<long long*>(smem + C::kSmemQ + C::kSmemKV + C::kXchgBytes + 1024);
+  uint32_t* s_trace = reinterpret_cast<uint32_t*>(smem + C::kSmemQ + C::kSmemKV + C::kXchgBytes + 256);
   if (trace_cta())
     for (int i = threadIdx.x; i < kTrEv * kTrSteps; i += blockDim.x) s_trace[i] = 0;
 #endif
@@ -296,6 +322,28 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_prefetch_4d(&tm_k, bx * 64, j * BN, hkv, b);
           tma_prefetch_4d(&tm_v, bx * 64, j * BN, hkv, b);
         }
+      if constexpr (kPSmem) {
+        // One barrier per ring slot; ring order = the issuer's consumption order:
+        // K_ulo, K_ulo+1, then (V_j, K_j+2) for every step j.
+        int it = 0;
+        auto load = [&](bool is_k, int jj) {
+          WAIT_L(&kv_empty[it % C::kStages], ((it / C::kStages) & 1) ^ 1);
+          uint64_t* bar = &kv_full[it % C::kStages];
+          mbar_arrive_expect_tx(bar, C::kKVTileBytes);
+          uint8_t* dst = sKV + (it % C::kStages) * C::kKVTileBytes;
+          for (int bx = 0; bx < C::kBoxes; ++bx)
+            tma_load_4d(is_k ? &tm_k : &tm_v, bar, dst + bx * BN * 128, bx * 64, jj * BN, hkv, b, pol_kv);
+          ++it;
+        };
+        if (uhi > ulo) {
+          load(true, ulo);
+          if (ulo + 1 < uhi) load(true, ulo + 1);
+          for (int j = ulo; j < uhi; ++j) {
+            load(false, j);
+            if (j + 2 < uhi) load(true, j + 2);
+          }
+        }
+      } else {
       // Load groups: g = 0 is K_ulo; g >= 1 is the pair (V_{ulo+g-1}, K_{ulo+g}) (the last
       // group has no K).  A group signals ONE "pair" barrier (kv_full[g % C::kPairBars]), so
       // the MMA issuer waits once per KV step for both tiles it needs next.
@@ -309,7 +357,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         const int it0 = g == 0 ? 0 : 2 * g - 1;          // ring index of the group's first tile
         const int it1 = g < n ? 2 * g : 2 * g - 1;       // ... and of its last tile
-        for (int it = it0; it <= it1; ++it) WAIT_LM(&kv_empty[it % C::kStages], ((it / C::kStages) & 1) ^ 1);
+        for (int it = it0; it <= it1; ++it) WAIT_L(&kv_empty[it % C::kStages], ((it / C::kStages) & 1) ^ 1);
         uint64_t* bar = &kv_full[g % C::kPairBars];
         mbar_arrive_expect_tx(bar, (it1 - it0 + 1) * C::kKVTileBytes);
         for (int it = it0; it <= it1; ++it) {
@@ -320,6 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int bx = 0; bx < C::kBoxes; ++bx)
             tma_load_4d(is_k ? &tm_k : &tm_v, bar, dst + bx * BN * 128, bx * 64, jj * BN, hkv, b, pol_kv);
         }
+      }
       }
     }
   } else if (warp == kWarpMma) {
@@ -362,6 +411,69 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit_warp(&o_done[t]);
       };
 
+      if constexpr (kPSmem) {
+        // Order per step j: PV0(j), QK0(j+2), PV1(j), QK1(j+2).  QK_t(i) overwrites
+        // S_t once the tile's softmax threads have loaded S_t(i-1) (barrier kBarS0+t).
+        auto wait_tile = [&](int it) {
+          WAIT_LM(&kv_full[it % C::kStages], (it / C::kStages) & 1);
+          tc_fence_after();
+        };
+        auto qk_p = [&](int t, int it, int i) {
+          if (i > rg[t].lo) {
+            named_bar_sync(kBarS0 + t, kTileThreads + 32);
+            tc_fence_after();
+          }
+          qk(t, it);
+        };
+        auto pv_p = [&](int t, int it, bool acc) {   // O_t += P_t V (P from shared memory)
+          named_bar_sync(kBarP0 + t, kTileThreads + 32);
+          tc_fence_after();
+          if (lane == 0) TRACE(13 + t, it / 2);
+          const uint32_t sp = smem_u32(sP + t * C::kPTileBytes);
+          const uint32_t sv = smem_u32(sKV + (it % C::kStages) * C::kKVTileBytes);
+#pragma unroll
+          for (int kk = 0; kk < BN / 16; ++kk) {
+            const uint32_t ka = (kk >> 2) * (BM * 128) + (kk & 3) * 32;
+            mma_ss_warp(tO[t], smem_desc_sw128(sp + ka, 16, 1024), smem_desc_sw128(sv + kk * 2048, BN * 128, 1024),
+                        idesc_pv, (acc || kk > 0) ? 1u : 0u);
+          }
+          mma_commit_warp(&o_done[t]);
+        };
+        int it = 0;
+        wait_tile(it);
+        if (active(rg[0], ulo)) qk_p(0, it, ulo);
+        if (active(rg[1], ulo)) qk_p(1, it, ulo);
+        mma_commit_warp(&kv_empty[it % C::kStages]);
+        ++it;
+        if (ulo + 1 < uhi) {
+          wait_tile(it);
+          if (active(rg[0], ulo + 1)) qk_p(0, it, ulo + 1);
+          if (active(rg[1], ulo + 1)) qk_p(1, it, ulo + 1);
+          mma_commit_warp(&kv_empty[it % C::kStages]);
+          ++it;
+        }
+        for (int j = ulo; j < uhi; ++j) {
+          const int itV = it++;
+          const bool k2 = j + 2 < uhi;
+          const int itK = k2 ? it++ : 0;
+          wait_tile(itV);
+          if (lane == 0) TRACE(12, j);
+          if (active(rg[0], j)) pv_p(0, itV, j > rg[0].lo);
+          if (lane == 0) TRACE(0, j);
+          if (k2) {
+            wait_tile(itK);
+            if (active(rg[0], j + 2)) qk_p(0, itK, j + 2);
+          }
+          if (lane == 0) TRACE(1, j);
+          if (active(rg[1], j)) pv_p(1, itV, j > rg[1].lo);
+          if (lane == 0) TRACE(2, j);
+          mma_commit_warp(&kv_empty[itV % C::kStages]);
+          if (k2) {
+            if (active(rg[1], j + 2)) qk_p(1, itK, j + 2);
+            mma_commit_warp(&kv_empty[itK % C::kStages]);
+          }
+        }
+      } else {
       wait_group(0);
       if (active(rg[0], ulo)) qk(0, 0);
       if (active(rg[1], ulo)) qk(1, 0);
@@ -382,6 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (active(rg[1], j + 1)) qk(1, itK1);
           mma_commit_warp(&kv_empty[itK1 % C::kStages]);
         }
+      }
       }
     }
   } else if (warp < kSoftmaxWarps) {
@@ -432,6 +545,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int c = 0; c < kHC / 32; ++c) tmem_ld32(tS + c * 32, reinterpret_cast<uint32_t(&)[32]>(u[c * 32]));
         tmem_ld_wait();
+        if constexpr (kPSmem) {
+          if (j + 1 < R.hi) {   // S_t is in registers: the issuer may compute S_t(j+1) into it
+            tc_fence_before();
+            named_bar_arrive(kBarS0 + t, kTileThreads + 32);
+          }
+        }
 #pragma unroll
         for (int c = 0; c < kHC; ++c) x[c] = u2f(u[c]);
       }
@@ -463,6 +582,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       // exp(x - m), local sum, P -> bf16 into TMEM (aliasing S)
       const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
       float m_use_t = m_use;
+      if constexpr (kPSmem) {
+        // PV_t(j-1) must be complete before P_t(j) overwrites sP_t
+        // (the rare O rescale stays after the exponentials, where the S registers are dead)
+        if (it > 0) {
+          mbar_wait(&o_done[t], (it - 1) & 1);
+          tc_fence_after();
+        }
+      }
       if (kToken) {
         named_bar_sync(t == 0 ? kBarTok0 : kBarTok1, 2 * kTileThreads);   // acquire the exp token
 #ifdef ATTN_TOKEN_STRICT
@@ -496,7 +623,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           sum1 += p1;
           pk[e] = pack2<kF16>(p0, p1);
         }
-        tmem_st16(tP + c0 / 2, pk);
+        if constexpr (kPSmem) {   // row r of P_t: K-major, 128-B swizzle (the UMMA A layout)
+          const int cc = c_base + c0;                      // S / P column of pk[0]
+          uint8_t* rowp = sP + t * C::kPTileBytes + (cc >> 6) * (BM * 128) + r * 128;
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const int ch = ((cc & 63) >> 3) + q4;
+            *reinterpret_cast<uint4*>(rowp + ((ch ^ (r & 7)) << 4)) =
+                make_uint4(pk[4 * q4], pk[4 * q4 + 1], pk[4 * q4 + 2], pk[4 * q4 + 3]);
+          }
+        } else {
+          tmem_st16(tP + c0 / 2, pk);
+        }
       }
 #ifdef ATTN_TOKEN_STRICT
       if (kToken) asm volatile("" ::"f"(sum0), "f"(sum1));
@@ -529,14 +667,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef ATTN_STRICT_WAITS
       // Sanitizer build: observe every o_done phase (the production kernel only
       // waits when it rescales O; it can never fall two phases behind).
-      if (it > 0 && !__any_sync(0xffffffffu, need_o)) {
+      if (!kPSmem && it > 0 && !__any_sync(0xffffffffu, need_o)) {
         mbar_wait(&o_done[t], (it - 1) & 1);
         tc_fence_after();
       }
 #endif
+      if constexpr (kPSmem) fence_proxy_async_smem();   // generic-proxy P stores -> tensor core reads
       tc_fence_before();
       if (t == 0 && lane == 0 && wt < 4) TRACE(20 + wq, j);
-      named_bar_arrive(kBarP0 + t, kTileThreads + 32);   // P_t(j) in TMEM -> MMA issuer
+      named_bar_arrive(kBarP0 + t, kTileThreads + 32);   // P_t(j) in TMEM / smem -> MMA issuer
     }
 
     // ------------------------------------------------------------ epilogue: O / l -> 16-bit -> TMA store
@@ -595,7 +734,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
 #ifdef ATTN_TRACE
   if (trace_cta())
-    for (int i = threadIdx.x; i < kTrEv * kTrSteps; i += blockDim.x) (&g_trace[0][0])[i] = s_trace[i];
+    for (int i = threadIdx.x; i < kTrEv * kTrSteps; i += blockDim.x)
+      g_trace[i / kTrSteps][i % kTrSteps] = s_trace[i];
 #endif
   if (warp == kWarpAlloc) {
     tc_fence_after();

@@ -15,5 +15,13 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:fwd_
   python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-decode > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:decode_split -s 2 -c 1 -o gpurun_out/prof_dec_$TAG \
   python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:softmax_rows -s 2 -c 1 -o gpurun_out/prof_smr_$TAG \
+  python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-decode > /dev/null 2>&1
+fi
+if [ -n "$SANITIZE" ]; then
+  for tool in memcheck racecheck synccheck; do
+    timeout 900 compute-sanitizer --tool $tool python tools/sanitize.py > gpurun_out/sanitize_${tool}_$TAG.log 2>&1
+    echo "rc=$?" >> gpurun_out/sanitize_${tool}_$TAG.log
+  done
 fi
 tail -3 gpurun_out/pytest_$TAG.log

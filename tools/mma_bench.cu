@@ -10,7 +10,7 @@
 
 using namespace attn;
 
-template <int N, bool kTS, int kAccum, int kLd, int kCopy = 0>
+template <int N, bool kTS, int kAccum, int kLd, int kCopy = 0, int kSt = 0>
 __global__ void __launch_bounds__(256, 1) bench(long long* out, int iters, const uint8_t* gsrc) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
@@ -26,7 +26,11 @@ __global__ void __launch_bounds__(256, 1) bench(long long* out, int iters, const
   tc_fence_after();
   const uint32_t tmem = tslot;
   __shared__ volatile int done;
-  if (threadIdx.x == 0) done = 0;
+  __shared__ unsigned long long st_bytes;
+  if (threadIdx.x == 0) {
+    done = 0;
+    st_bytes = 0;
+  }
   __syncthreads();
   if (kLd && warp >= 4) {
     // TMEM readers (like softmax warps): 32x32b.x32 loads of columns [256, 384) until the MMAs finish
@@ -41,6 +45,26 @@ __global__ void __launch_bounds__(256, 1) bench(long long* out, int iters, const
       }
     }
     if (acc == 12345.f) out[0] = 1;
+  }
+  if (kSt && warp >= 4) {
+    // softmax-like P stores: each thread writes 16-B vectors of its 256-B row into
+    // [96 KB, 160 KB) with the 128-B swizzle, until the MMAs finish
+    const int row = (warp & 3) * 32 + (threadIdx.x & 31);
+    uint8_t* base = smem + 98304 + (kSt == 2 ? 0 : 0);
+    unsigned long long n = 0;
+    uint4 v = make_uint4(row, 1, 2, 3);
+    while (!done) {
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const int chunk = c & 7, half = c >> 3;
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(base + half * 16384 + row * 128 + ((chunk ^ (row & 7)) * 16))),
+                     "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+        v.y += 1;
+      }
+      n += 256;
+      if (kSt == 2) __nanosleep(200);
+    }
+    atomicAdd(&st_bytes, n);
   }
   __shared__ uint64_t cbar;
   __shared__ long long copy_bytes;
@@ -83,6 +107,7 @@ __global__ void __launch_bounds__(256, 1) bench(long long* out, int iters, const
   }
   __syncthreads();
   if (kCopy && threadIdx.x == 0) out[148 + blockIdx.x] = copy_bytes;
+  if (kSt && threadIdx.x == 0) out[296 + blockIdx.x] = st_bytes;
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
@@ -91,21 +116,22 @@ __global__ void __launch_bounds__(256, 1) bench(long long* out, int iters, const
   }
 }
 
-template <int N, bool kTS, int kAccum, int kLd = 0, int kCopy = 0>
+template <int N, bool kTS, int kAccum, int kLd = 0, int kCopy = 0, int kSt = 0>
 void run(const char* name, long long* d_out) {
   const int iters = 2000;
-  auto k = bench<N, kTS, kAccum, kLd, kCopy>;
+  auto k = bench<N, kTS, kAccum, kLd, kCopy, kSt>;
   static uint8_t* g = nullptr;
   if (!g) cudaMalloc(&g, 148u << 20);
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-  k<<<148, 256, 96 * 1024>>>(d_out, 10, g);
-  k<<<148, 256, 96 * 1024>>>(d_out, iters, g);
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  k<<<148, 256, 160 * 1024>>>(d_out, 10, g);
+  k<<<148, 256, 160 * 1024>>>(d_out, iters, g);
   cudaError_t e = cudaDeviceSynchronize();
-  std::vector<long long> h(296);
-  cudaMemcpy(h.data(), d_out, 296 * 8, cudaMemcpyDeviceToHost);
-  double avg = 0, cb = 0;
-  for (int i = 0; i < 148; ++i) { avg += h[i]; cb += h[148 + i]; }
-  avg /= 148; cb /= 148;
+  std::vector<long long> h(444);
+  cudaMemcpy(h.data(), d_out, 444 * 8, cudaMemcpyDeviceToHost);
+  double avg = 0, cb = 0, sb = 0;
+  for (int i = 0; i < 148; ++i) { avg += h[i]; cb += h[148 + i]; sb += h[296 + i]; }
+  avg /= 148; cb /= 148; sb /= 148;
+  if (kSt) printf("   st.shared: %.1f B/clk per SM during the MMAs\n", sb / avg);
   if (kCopy) printf("   copy: %.1f B/clk per SM during the MMAs\n", cb / avg);
   const double mmas = iters * 8.0;
   printf("%-28s %s  cycles/MMA %.1f  (ideal %.0f)  flop/clk/SM %.0f\n", name, cudaGetErrorString(e), avg / mmas,
@@ -114,7 +140,8 @@ void run(const char* name, long long* d_out) {
 
 int main() {
   long long* d;
-  cudaMalloc(&d, 296 * 8);
+  cudaMalloc(&d, 444 * 8);
+  cudaMemset(d, 0, 444 * 8);
   run<128, false, 1>("SS M128 N128 K16", d);
   run<256, false, 1>("SS M128 N256 K16", d);
   run<128, true, 1>("TS M128 N128 K16 (A tmem)", d);
@@ -124,5 +151,9 @@ int main() {
   run<128, true, 1, 1>("TS N128 + 4 LDTM warps", d);
   run<128, false, 1, 0, 1>("SS N128 + bulk copies", d);
   run<128, true, 1, 0, 1>("TS N128 + bulk copies", d);
+  run<128, false, 1, 0, 0, 1>("SS N128 + 4 warps st.shared", d);
+  run<128, true, 1, 0, 0, 1>("TS N128 + 4 warps st.shared", d);
+  run<128, false, 1, 0, 1, 1>("SS N128 + copies + st.shared", d);
+  run<128, false, 1, 0, 1, 2>("SS N128 + copies + paced st", d);
   return 0;
 }

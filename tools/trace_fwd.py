@@ -3,7 +3,7 @@ import ctypes, os, subprocess, sys
 import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-lib_path = os.path.join(ROOT, "build", "libattn_trace.so")
+lib_path = os.path.join(ROOT, "build", "libattn_trace%s.so" % os.environ.get("TRACE_TAG", ""))
 if not os.path.exists(lib_path):
     src = [os.path.join(ROOT, "paper_2510_08726_b200", "csrc", f) for f in ("api.cu", "fwd_tc.cu", "fwd_simt.cu", "decode.cu", "softmax_rows.cu")]
     subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -26,4 +26,4 @@ names = {12: "mma:V ready", 13: "mma:P0 seen", 15: "mma:K+1 ready", 14: "mma:P1 
          6: "sm0:token", 7: "sm0:P done", 8: "sm1:wait S", 9: "sm1:S ready", 10: "sm1:token", 11: "sm1:P done", 16: "w4 exp end", 17: "w5 exp end", 18: "w6 exp end", 19: "w7 exp end", 20: "w4 arrive", 21: "w5 arrive", 22: "w6 arrive", 23: "w7 arrive", 24: "ld:K issue", 25: "ld:V issue"}
 print("step " + " ".join(f"{names[e]:>13s}" for e in names))
 for j in range(33):
-    print(f"{j:4d} " + " ".join(f"{(tr[e, j] - t0) if tr[e, j] else 0:13d}" for e in names))
+    print(f"{j:4d} " + " ".join(f"{((tr[e, j] - t0) & 0xffffffff) if tr[e, j] else 0:13d}" for e in names))
