@@ -274,13 +274,14 @@ def main_gpu(args):
     flops = 4.0 * D * allowed_pairs(S, var) * B * Hq
     value = world * flops / (ms * 1e-3) / 1e12
     achieved = flops / (ms * 1e-3) / 1e12
-    traffic, traffic_decode = None, None
+    traffic, traffic_decode, traffic_smr = None, None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
             tr = json.load(open(tpath))
             traffic = tr.get(f"fwd_{name}")
             traffic_decode = tr.get(f"decode_b{args.decode_batch}") if world == 1 else None
+            traffic_smr = tr.get("softmax_rows")
         except Exception:
             traffic = None
     line = {
@@ -385,7 +386,7 @@ def main_gpu(args):
             "unit": "GB/s", "ms_per_step": sms, "scaling": "weak" if world > 1 else None,
             "config": {"workload": "softmax rows (NEXT-4)", "rows": rows, "cols": cols, "dtype": "bf16"},
             "roofline": {"bound": "hbm", "achieved": sgbs, "peak": peaks["hbm"], "unit": "GB/s",
-                         "frac": sgbs / peaks["hbm"], "traffic": None, "kernel": "softmax_rows_kernel",
+                         "frac": sgbs / peaks["hbm"], "traffic": traffic_smr, "kernel": "softmax_rows16_kernel",
                          "algorithmic_bytes_per_launch": sbytes},
         }
         del xs, ys
