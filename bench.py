@@ -331,7 +331,7 @@ def main_gpu(args):
                     dgd.fill_(kd[b, h], seed5, 2, start=start)
                     dgd.fill_(vd[b, h], seed5, 3, start=start)
             od = torch.empty_like(qd)
-            ws = torch.empty(pb.workspace_bytes(qd, kd), dtype=torch.uint8, device=dev)
+            ws = torch.zeros(pb.workspace_bytes(qd, kd), dtype=torch.uint8, device=dev)  # ticket block must start at 0
             if world == 1:
                 dstep = lambda: pb.splitkv_decode(qd, kd, vd, causal=True, out=od, workspace=ws)  # noqa: E731
             else:

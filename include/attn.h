@@ -147,7 +147,12 @@ ATTN_API attn_status attn_fused_fwd(const attn_problem* prob, attn_tensor q, att
  * attn_splitkv_default_splits: split count used when num_splits == 0
  *   (enough (b, hkv, split) units to fill sm_count SMs).
  * attn_splitkv_workspace_bytes: DEVICE workspace needed to hold the
- *   partials when parts_out == NULL (pure host function).
+ *   partials when parts_out == NULL (pure host function).  Its FIRST
+ *   256-byte-rounded [B][Hkv] uint32 block holds the arrival tickets of the
+ *   fused global section and MUST be zero before the call (e.g. cudaMemset
+ *   once); every completed call leaves it zero, so a workspace reused for the
+ *   same or a smaller B*Hkv needs no further clearing.  One workspace serves
+ *   one stream at a time.
  * Part s covers local keys [s*L, min((s+1)*L, seqlen_kv)) with
  *   L = 64 * ceil(ceil(seqlen_kv / num_splits) / 64)   (trailing parts may be
  *   empty: m = -inf, l = 0, O = 0).
@@ -155,6 +160,11 @@ ATTN_API attn_status attn_fused_fwd(const attn_problem* prob, attn_tensor q, att
  *   (parts_out->num_parts must equal the split count) and no workspace is
  *   needed; if o != NULL the normalised output (q's dtype) and lse (nullable)
  *   are written after the combine.  At least one of parts_out / o must be set.
+ *   With parts_out == NULL and o != NULL the global section runs INSIDE the
+ *   split kernel: each CTA publishes its triples and takes a ticket; the last
+ *   CTA of the (b, hkv) group combines all splits (Eq. 8) -- one launch.
+ *   (If num_splits is too large for the kernel to stage the per-split
+ *   weights, or parts_out is given, a separate combine launch is used.)
  * ------------------------------------------------------------------- */
 ATTN_API int32_t attn_splitkv_default_splits(const attn_problem* prob, int32_t sm_count);
 ATTN_API size_t attn_splitkv_workspace_bytes(const attn_problem* prob, int32_t num_splits);

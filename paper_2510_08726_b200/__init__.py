@@ -142,6 +142,26 @@ def workspace_bytes(q: torch.Tensor, k: torch.Tensor, num_splits: int = 0) -> in
     return load().attn_splitkv_workspace_bytes(ctypes.byref(prob), num_splits)
 
 
+_WS_CACHE = {}
+
+
+def _decode_workspace(device, need: int, ticket_bytes: int, stream) -> torch.Tensor:
+    """Per-(device, stream) decode workspace.  Its leading ticket block must be zero
+    before a call and every call leaves it zero (include/attn.h), so only a ticket
+    block larger than any before it (which may overlap old partials) is cleared."""
+    key = (device.index if device.index is not None else torch.cuda.current_device(), _stream(stream).value)
+    ws, clean = _WS_CACHE.get(key, (None, 0))
+    if ws is None or ws.numel() < need:
+        ws = torch.zeros(max(need, 1 << 20), dtype=torch.uint8, device=device)
+        clean = ws.numel()
+    if ticket_bytes > clean:
+        ws[:ticket_bytes].zero_()
+    if stream is not None:
+        stream.wait_stream(torch.cuda.current_stream(device))
+    _WS_CACHE[key] = (ws, ticket_bytes)   # after the call: tickets zero, partials beyond dirty
+    return ws
+
+
 def splitkv_decode(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, num_splits: int = 0,
                    scale: Optional[float] = None, causal: bool = False, window: Tuple[int, int] = (-1, -1),
                    alibi_slopes: Optional[torch.Tensor] = None, softcap: float = 0.0,
@@ -152,7 +172,9 @@ def splitkv_decode(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, num_spl
     """Split-K Update decode (``attn_splitkv_decode``): q [B, Hq, 1, D] bf16.
 
     ``parts`` receives the raw local-section triples; with ``want_out`` the
-    Eq. 8 combine also produces O (and lse)."""
+    Eq. 8 combine also produces O (and lse) -- fused into the split kernel
+    when ``parts`` is None.  A caller-supplied ``workspace`` must be zeroed
+    before its first use (its ticket block; include/attn.h)."""
     lib = load()
     if q.device.type == "cpu":
         dev = torch.device("cuda", torch.cuda.current_device())
@@ -179,7 +201,8 @@ def splitkv_decode(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, num_spl
     if parts is None:
         need = lib.attn_splitkv_workspace_bytes(ctypes.byref(prob), num_splits)
         if workspace is None or workspace.numel() * workspace.element_size() < need:
-            workspace = torch.empty(need, dtype=torch.uint8, device=q.device)
+            tb = (q.shape[0] * k.shape[1] * 4 + 255) // 256 * 256
+            workspace = _decode_workspace(q.device, need, tb, stream)
         ws_ptr, ws_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
     cparts = None if parts is None else ctypes.byref(parts.c())
     check(lib.attn_splitkv_decode(ctypes.byref(prob), _as_tensor(q), _as_tensor(k), _as_tensor(v), num_splits,

@@ -221,7 +221,8 @@ size_t attn_splitkv_workspace_bytes(const attn_problem* p, int32_t num_splits) {
   if (num_splits <= 0) num_splits = attn_splitkv_default_splits(p, 0);
   const size_t rows = (size_t)num_splits * p->batch * p->heads_q;
   auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
-  return up(rows * 4) * 2 + up(rows * p->head_dim * 4);
+  // the fused combine's arrival tickets [B][Hkv] (zero between calls), then m | l | O partials
+  return up((size_t)p->batch * p->heads_kv * 4) + up(rows * 4) * 2 + up(rows * p->head_dim * 4);
 }
 
 attn_status attn_splitkv_decode(const attn_problem* prob, attn_tensor q, attn_tensor k, attn_tensor v,
@@ -246,7 +247,7 @@ attn_status attn_splitkv_decode(const attn_problem* prob, attn_tensor q, attn_te
   if ((st = check_tensor(v, "v", 2, p.batch, p.heads_kv, p.seqlen_kv)) != ATTN_OK) return st;
   if (o.ptr != nullptr && (st = check_tensor(o, "o", 2, p.batch, p.heads_q, 1)) != ATTN_OK) return st;
 
-  attn::DecodeArgs a;
+  attn::DecodeArgs a{};
   a.s = shape_of(prob);
   a.f16 = p.dtype == ATTN_FP16;
   a.v = vp;
@@ -270,13 +271,24 @@ attn_status attn_splitkv_decode(const attn_problem* prob, attn_tensor q, attn_te
       return fail(ATTN_ERR_WORKSPACE_TOO_SMALL, "workspace needs %zu bytes", need);
     const size_t rows = (size_t)num_splits * p.batch * p.heads_q;
     auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
-    char* w = static_cast<char*>(workspace);
+    char* const w0 = static_cast<char*>(workspace);
+    char* w = w0 + up((size_t)p.batch * p.heads_kv * 4);   // after the ticket block
     float* m = reinterpret_cast<float*>(w);
     float* l = reinterpret_cast<float*>(w + up(rows * 4));
     float* ob = reinterpret_cast<float*>(w + 2 * up(rows * 4));
     const long long bh = (long long)p.batch * p.heads_q;
     a.parts = attn::PartsView{m, l, ob, num_splits, bh, p.heads_q, 1, bh * p.head_dim,
                               (long long)p.heads_q * p.head_dim, p.head_dim};
+    // Fused Eq. 8 combine (last CTA per (b, hkv)) when the output is wanted and the
+    // split weights fit the kernel's staging area; else the separate combine kernel.
+    if (o.ptr != nullptr && num_splits <= attn::decode_fused_max_splits(G, p.head_dim)) {
+      a.tickets = reinterpret_cast<unsigned*>(w0);
+      a.out_f16 = p.dtype == ATTN_FP16 ? 1 : 0;
+      a.o = o.ptr;
+      a.o_sb = o.stride_b;
+      a.o_sh = o.stride_h;
+      a.lse = lse;
+    }
   }
   if ((st = make_map(&a.tm_k, k, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, nk, true, a.f16)) != ATTN_OK) return st;
   if ((st = make_map(&a.tm_v, v, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, nk, true, a.f16)) != ATTN_OK) return st;
@@ -284,7 +296,7 @@ attn_status attn_splitkv_decode(const attn_problem* prob, attn_tensor q, attn_te
   int launches = 0;
   st = cuda_status(attn::launch_decode(a, s, &launches), "decode launch");
   if (st != ATTN_OK) return st;
-  if (o.ptr != nullptr) {
+  if (o.ptr != nullptr && a.tickets == nullptr) {
     attn::CombineArgs c{};
     c.B = p.batch;
     c.H = p.heads_q;

@@ -274,6 +274,59 @@ __global__ void __launch_bounds__(kThreads) decode_split_kernel(const __grid_con
       a.parts.l[mi] = L;
     }
   }
+  if (a.tickets == nullptr) return;
+
+  // ------------------------------------------------------------ fused global section (Eq. 8)
+  // Every CTA publishes its triples (fence, then one ticket per CTA); the last of the
+  // (b, hkv) group reads all splits back from L2 and combines them: no second launch.
+  __shared__ int s_last;
+  __threadfence();
+  named_bar_sync(1, kConsumerWarps * 32);
+  unsigned* ticket = a.tickets + (long long)b * a.s.Hkv + hkv;
+  if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == (unsigned)a.num_splits - 1;
+  named_bar_sync(1, kConsumerWarps * 32);
+  if (!s_last) return;
+  __threadfence();
+  const int S = a.num_splits;
+  float* wts = red;                       // [G][S] weights exp(m_s - M) / L (smem reused)
+  float* stat = red + G * S;              // [G][2]: M (natural log), L
+  for (int h = warp; h < G; h += kConsumerWarps) {   // warp reduces head h over the splits
+    const int hh = hkv * G + h;
+    const long long mb = (long long)b * a.parts.m_sb + (long long)hh * a.parts.m_sh;
+    float M = -INFINITY;
+    for (int sp = lane; sp < S; sp += 32) M = fmaxf(M, __ldcg(a.parts.m + sp * a.parts.m_sp + mb));
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o2));
+    float L = 0.f;
+    for (int sp = lane; sp < S; sp += 32) {
+      const float ms = __ldcg(a.parts.m + sp * a.parts.m_sp + mb);
+      const float w = (ms == -INFINITY) ? 0.f : expf(ms - M);   // repair term exp(max_s - max_g)
+      wts[h * S + sp] = w;
+      L = fmaf(w, __ldcg(a.parts.l + sp * a.parts.m_sp + mb), L);
+    }
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o2);
+    if (lane == 0) {
+      stat[h * 2] = M;
+      stat[h * 2 + 1] = L;
+    }
+  }
+  named_bar_sync(1, kConsumerWarps * 32);
+  for (int e = threadIdx.x; e < G * D; e += kConsumerWarps * 32) {
+    const int h = e / D, d = e % D;
+    const int hh = hkv * G + h;
+    const float L = stat[h * 2 + 1];
+    const float* po = a.parts.o + (long long)b * a.parts.o_sb + (long long)hh * a.parts.o_sh + d;
+    float acc = 0.f;
+    if (L > 0.f)
+      for (int sp = 0; sp < S; ++sp) acc = fmaf(wts[h * S + sp], __ldcg(po + sp * a.parts.o_sp), acc);
+    const float out = L > 0.f ? acc / L : 0.f;
+    const long long oi = (long long)b * a.o_sb + (long long)hh * a.o_sh + d;
+    if (a.out_f16) reinterpret_cast<__half*>(a.o)[oi] = __float2half_rn(out);
+    else reinterpret_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(out);
+    if (d == 0 && a.lse) a.lse[(long long)b * a.s.Hq + hh] = L > 0.f ? stat[h * 2] + logf(L) : -INFINITY;
+  }
+  if (threadIdx.x == 0) *ticket = 0u;     // ready for the next call
 }
 
 // ---------------------------------------------------------------- Eq. 8 combine
@@ -412,6 +465,11 @@ cudaError_t launch_dec_d(const DecodeArgs& a, cudaStream_t stream) {
 }  // namespace
 
 int decode_stage_keys(int, int) { return NK; }
+int decode_fused_max_splits(int G, int D) {
+  // the fused combine stages [G][S] weights + [G][2] stats in the (then idle) stage ring
+  const int bytes = kStages * 2 * NK * D * 2;
+  return bytes / (4 * G) - 2;
+}
 
 cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t stream, int* launches) {
   cudaError_t e = a.f16 ? (a.s.D == 128 ? launch_dec_d<128, true>(a, stream) : launch_dec_d<64, true>(a, stream))

@@ -268,6 +268,38 @@ def test_decode_full_config_sampled(B):
     assert_bf16_close(np.concatenate(got), np.concatenate(ref), f"decode B={B}")
 
 
+@pytest.mark.parametrize("case", range(len(DECODE_CASES)))
+def test_decode_fused_combine(case):
+    """parts=None: the Eq. 8 global section runs inside the split kernel (last CTA per
+    (b, hkv) combines, one launch).  Same output as the two-launch path, equal to the
+    oracle, and the ticket block is back to zero after every call (include/attn.h)."""
+    c = dict(DECODE_CASES[case])
+    B, Hq, Hkv, Skv, D, splits = (c.pop(k) for k in ("B", "Hq", "Hkv", "Skv", "D", "splits"))
+    if c.pop("alibi", False):
+        c["alibi_slopes"] = datagen.alibi_slopes(Hq)
+    p = problem(B, Hq, Hkv, 1, Skv, D, **c)
+    raw, (q64, k64, v64) = gen_qkv(500 + case, B, Hq, Hkv, 1, Skv, D)
+    ref_o, ref_l = oracle.attention(p, q64, k64, v64)
+    q, k, v = (dgd.to_device(x) for x in raw)
+    kw = _kw_from(p)
+    ws = torch.zeros(pb.workspace_bytes(q, k, splits), dtype=torch.uint8, device="cuda")
+    outs = []
+    for _ in range(3):   # the same workspace three times: tickets must reset
+        o, lse = pb.splitkv_decode(q, k, v, num_splits=splits, workspace=ws, return_lse=True, **kw)
+        torch.cuda.synchronize()
+        assert pb.last_launch_count() == 1
+        outs.append(o.clone())
+        tickets = ws[:(B * Hkv * 4 + 255) // 256 * 256]
+        assert int(tickets.count_nonzero()) == 0
+    assert_bf16_close(_bf16_np(outs[0]), ref_o, f"fused decode case {case}")
+    assert_lse_close(lse.cpu().numpy(), ref_l[:, :, 0], LSE_TOL_BF16, "fused decode lse")
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+    parts = pb.Parts.empty(splits, B, Hq, D, "cuda")
+    o2 = pb.splitkv_decode(q, k, v, num_splits=splits, parts=parts, **kw)   # two-launch path
+    torch.cuda.synchronize()
+    assert (o2.float() - outs[0].float()).abs().max().item() <= 2 ** -7
+
+
 def test_combine_kernel_matches_oracle():
     """attn_combine alone on oracle-made partials, with empty (-inf) parts and
     an un-normalised acc output merged again (hierarchical, R3)."""
