@@ -144,8 +144,9 @@ ATTN_API attn_status attn_fused_fwd(const attn_problem* prob, attn_tensor q, att
  * partial triple per (part, b, hq).  Then the global section (Eq. 8)
  * combines them (attn_combine).
  *
- * attn_splitkv_default_splits: split count used when num_splits == 0
- *   (enough (b, hkv, split) units to fill sm_count SMs).
+ * attn_splitkv_default_splits: split count used when num_splits == 0: the
+ *   largest count with at most one (b, hkv, split) CTA per SM (>= 1; sm_count
+ *   <= 0 means the current device's).
  * attn_splitkv_workspace_bytes: DEVICE workspace needed to hold the
  *   partials when parts_out == NULL (pure host function).  Its FIRST
  *   256-byte-rounded [B][Hkv] uint32 block holds the arrival tickets of the

@@ -208,8 +208,10 @@ int32_t attn_splitkv_default_splits(const attn_problem* p, int32_t sm_count) {
   if (sm_count <= 0) sm_count = sm_count_cached();
   const int nk = attn::decode_stage_keys(p->heads_q / p->heads_kv, p->head_dim);
   const int64_t units = (int64_t)p->batch * p->heads_kv;
-  const int64_t target = 2LL * sm_count;   // two resident CTAs per SM
-  int64_t splits = (target + units - 1) / units;
+  // The largest split count with at most ONE (b, hkv, split) CTA per SM: measured on B200
+  // (tools/decode_splits.py) this streams K/V fastest (B = 1..16: 6.2-7.2 TB/s), while two
+  // per SM or a partial second wave lose 5-20 %.
+  int64_t splits = sm_count / units;
   const int64_t max_splits = (p->seqlen_kv + nk - 1) / nk;
   if (splits > max_splits) splits = max_splits;
   if (splits < 1) splits = 1;

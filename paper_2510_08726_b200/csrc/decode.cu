@@ -32,7 +32,10 @@ namespace {
 constexpr int kConsumerWarps = 4;
 constexpr int kKeysPerWarp = 16;
 constexpr int NK = kConsumerWarps * kKeysPerWarp;  // keys per stage
-constexpr int kStages = 3;
+#ifndef DEC_STAGES
+#define DEC_STAGES 3
+#endif
+constexpr int kStages = DEC_STAGES;   // K+V ring stages (32 KiB each at D = 128)
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kLog2e = 1.4426950408889634f;

@@ -106,7 +106,7 @@ def test_decode_errors(lib):
 def test_workspace_and_splits_are_host_functions(lib):
     p = _prob(seqlen_q=1, batch=1, heads_q=32, heads_kv=8, seqlen_kv=131072)
     s = lib.attn_splitkv_default_splits(ctypes.byref(p), 148)
-    assert 1 <= s <= 131072 // 64 and s * 8 >= 148          # fills the GPU
+    assert s == 148 // 8                                    # one CTA per SM, one wave
     ws = lib.attn_splitkv_workspace_bytes(ctypes.byref(p), s)
     assert ws >= s * 32 * (128 + 2) * 4
     p.seqlen_kv = 10
