@@ -70,7 +70,8 @@ typedef enum {
   ATTN_ERR_UNSUPPORTED = 2,
   ATTN_ERR_ALIGNMENT = 3,
   ATTN_ERR_WORKSPACE_TOO_SMALL = 4,
-  ATTN_ERR_CUDA = 5
+  ATTN_ERR_CUDA = 5,
+  ATTN_ERR_NCCL = 6 /* NCCL missing (libnccl.so.2 not loadable) or an NCCL call failed */
 } attn_status;
 
 typedef enum {
@@ -228,6 +229,41 @@ ATTN_API attn_status attn_merge_partials(int32_t num_parts, int64_t rows, int32_
 ATTN_API attn_status attn_softmax_rows(int64_t rows, int32_t cols, attn_dtype dtype, const void* x,
                                        int64_t x_stride_row, void* y, int64_t y_stride_row, float* row_max,
                                        float* row_sum, attn_stream_t stream);
+
+/* ---------------------------------------------------------------------
+ * Multi-GPU Split-K decode over a KV-SEQUENCE-sharded cache (
+ * the same Eq. 8 algebra one level up, valid by Eq. 4).  One
+ * process per GPU; NCCL is loaded at run time (dlopen "libnccl.so.2", so a
+ * process that already loaded torch's NCCL shares it).
+ *
+ * attn_nccl_get_unique_id: writes the 128-byte ncclUniqueId (rank 0 calls it
+ *   and ships the bytes to the other ranks out of band).
+ * attn_nccl_comm_init: *comm = a new communicator handle (host memory) over
+ *   nranks processes; this process is `rank`; the CURRENT CUDA device is
+ *   used.  Blocks until all ranks joined (ncclCommInitRank).
+ * attn_nccl_comm_destroy: frees the handle (NULL is a no-op).
+ * attn_decode_kv_sharded_workspace_bytes: DEVICE workspace for the call below.
+ * attn_decode_kv_sharded: `local` describes THIS rank's shard: seqlen_kv =
+ *   shard length, kv_pos_offset = absolute position of the shard's first key,
+ *   seqlen_kv_total = global KV length; q is replicated on every rank.  Steps,
+ *   all enqueued on `stream`:
+ *     1. attn_splitkv_decode over the shard -> split triples (workspace);
+ *     2. attn_combine -> one UN-normalised triple per (b, hq), packed as
+ *        [B][Hq][D+2] fp32 (O at 0..D-1, m at D, l at D+1);
+ *     3. ncclAllGather -> [nranks][B][Hq][D+2];
+ *     4. attn_combine over the nranks parts -> o (q's dtype), lse (nullable,
+ *        fp32 [B][Hq]) -- identical on every rank.
+ *   Errors: those of attn_splitkv_decode / attn_combine, WORKSPACE_TOO_SMALL,
+ *   NCCL.
+ * ------------------------------------------------------------------- */
+ATTN_API attn_status attn_nccl_get_unique_id(void* id_out);
+ATTN_API attn_status attn_nccl_comm_init(void** comm, int32_t nranks, int32_t rank, const void* nccl_unique_id);
+ATTN_API attn_status attn_nccl_comm_destroy(void* comm);
+ATTN_API size_t attn_decode_kv_sharded_workspace_bytes(const attn_problem* local, int32_t nranks);
+ATTN_API attn_status attn_decode_kv_sharded(void* comm, const attn_problem* local, attn_tensor q,
+                                            attn_tensor k_shard, attn_tensor v_shard, void* workspace,
+                                            size_t workspace_bytes, attn_tensor o, float* lse,
+                                            attn_stream_t stream);
 
 /* ---------------------------------------------------------------------
  * Seeded synthetic inputs are produced by a separate library (datagen/);

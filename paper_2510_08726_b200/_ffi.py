@@ -15,6 +15,7 @@ ATTN_ERR_UNSUPPORTED = 2
 ATTN_ERR_ALIGNMENT = 3
 ATTN_ERR_WORKSPACE_TOO_SMALL = 4
 ATTN_ERR_CUDA = 5
+ATTN_ERR_NCCL = 6
 ATTN_BF16 = 0
 ATTN_FP32 = 1
 ATTN_FP16 = 2
@@ -22,7 +23,9 @@ ATTN_Q_POS_DEFAULT = -(1 << 63)
 
 EXPORTED = ("attn_fused_fwd", "attn_splitkv_default_splits", "attn_splitkv_workspace_bytes",
             "attn_splitkv_decode", "attn_combine", "attn_status_string", "attn_last_error",
-            "attn_abi_version", "attn_last_launch_count", "attn_merge_partials", "attn_softmax_rows")
+            "attn_abi_version", "attn_last_launch_count", "attn_merge_partials", "attn_softmax_rows",
+            "attn_nccl_get_unique_id", "attn_nccl_comm_init", "attn_nccl_comm_destroy",
+            "attn_decode_kv_sharded_workspace_bytes", "attn_decode_kv_sharded")
 
 
 class AttnTensor(ctypes.Structure):
@@ -76,6 +79,16 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.attn_merge_partials.restype = ctypes.c_int
     lib.attn_softmax_rows.argtypes = [i64, i32, ctypes.c_int, vp, i64, vp, i64, vp, vp, vp]
     lib.attn_softmax_rows.restype = ctypes.c_int
+    lib.attn_nccl_get_unique_id.argtypes = [vp]
+    lib.attn_nccl_get_unique_id.restype = ctypes.c_int
+    lib.attn_nccl_comm_init.argtypes = [ctypes.POINTER(ctypes.c_void_p), i32, i32, vp]
+    lib.attn_nccl_comm_init.restype = ctypes.c_int
+    lib.attn_nccl_comm_destroy.argtypes = [vp]
+    lib.attn_nccl_comm_destroy.restype = ctypes.c_int
+    lib.attn_decode_kv_sharded_workspace_bytes.argtypes = [P, i32]
+    lib.attn_decode_kv_sharded_workspace_bytes.restype = ctypes.c_size_t
+    lib.attn_decode_kv_sharded.argtypes = [vp, P, T, T, T, vp, ctypes.c_size_t, T, f32p, vp]
+    lib.attn_decode_kv_sharded.restype = ctypes.c_int
     lib.attn_status_string.argtypes = [ctypes.c_int]
     lib.attn_status_string.restype = ctypes.c_char_p
     lib.attn_last_error.restype = ctypes.c_char_p

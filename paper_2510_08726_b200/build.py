@@ -27,6 +27,7 @@ LIBS = {
     os.path.join(PKG, "libattn.so"): {
         "sources": [os.path.join(CSRC, f) for f in ("api.cu", "fwd_tc.cu", "fwd_simt.cu", "decode.cu", "softmax_rows.cu")],
         "headers": [os.path.join(CSRC, f) for f in ("ptx.cuh", "kernels.h")] + [os.path.join(ROOT, "include", "attn.h")],
+        "link": ["-ldl"],   # NCCL is dlopen'ed (multi-GPU decode), never linked
     },
     os.path.join(ROOT, "datagen", "libdatagen.so"): {
         "sources": [os.path.join(ROOT, "datagen", "gen.cu")],
@@ -67,7 +68,7 @@ def build(verbose: bool = False, extra_flags=()) -> list[str]:
                 if verbose and log:
                     sys.stderr.write(log)
         if jobs or _stale(lib, objs):
-            _run([NVCC, *ARCH, "-shared", "-o", lib, *objs])
+            _run([NVCC, *ARCH, "-shared", "-o", lib, *objs, *spec.get("link", [])])
         built.append(lib)
     return built
 

@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include <dlfcn.h>
+
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -152,6 +154,7 @@ const char* attn_status_string(attn_status s) {
     case ATTN_ERR_ALIGNMENT: return "alignment";
     case ATTN_ERR_WORKSPACE_TOO_SMALL: return "workspace too small";
     case ATTN_ERR_CUDA: return "cuda error";
+    case ATTN_ERR_NCCL: return "nccl error";
   }
   return "unknown status";
 }
@@ -400,6 +403,129 @@ attn_status attn_softmax_rows(int64_t rows, int32_t cols, attn_dtype dtype, cons
                                "softmax_rows launch");
   if (st == ATTN_OK) g_launches = launches;
   return st;
+}
+
+// ---------------------------------------------------------------- multi-GPU decode (NCCL, loaded at run time)
+namespace {
+struct NcclApi {
+  using Uid = struct { char internal[128]; };
+  int (*get_unique_id)(Uid*) = nullptr;
+  int (*comm_init_rank)(void** comm, int nranks, Uid id, int rank) = nullptr;
+  int (*comm_destroy)(void* comm) = nullptr;
+  int (*all_gather)(const void* send, void* recv, size_t count, int dtype, void* comm, cudaStream_t s) = nullptr;
+  const char* (*error_string)(int) = nullptr;
+  bool ok = false;
+};
+const NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    api.all_gather = reinterpret_cast<decltype(api.all_gather)>(dlsym(h, "ncclAllGather"));
+    api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+    api.ok = api.get_unique_id && api.comm_init_rank && api.comm_destroy && api.all_gather && api.error_string;
+  });
+  return api;
+}
+struct Comm {
+  void* nc;
+  int nranks, rank;
+};
+constexpr int kNcclFloat32 = 7;   // ncclFloat32 in nccl.h's ncclDataType_t
+attn_status nccl_status(int r, const char* what) {
+  if (r == 0) return ATTN_OK;
+  return fail(ATTN_ERR_NCCL, "%s: %s", what, nccl().error_string ? nccl().error_string(r) : "?");
+}
+size_t up256(size_t x) { return (x + 255) & ~size_t(255); }
+}  // namespace
+
+attn_status attn_nccl_get_unique_id(void* id_out) {
+  g_err[0] = 0;
+  CHECK_ARG(id_out != nullptr, "id_out is NULL");
+  if (!nccl().ok) return fail(ATTN_ERR_NCCL, "libnccl.so.2 not loadable");
+  NcclApi::Uid id;
+  attn_status st = nccl_status(nccl().get_unique_id(&id), "ncclGetUniqueId");
+  if (st == ATTN_OK) memcpy(id_out, id.internal, sizeof(id.internal));
+  return st;
+}
+
+attn_status attn_nccl_comm_init(void** comm, int32_t nranks, int32_t rank, const void* nccl_unique_id) {
+  g_err[0] = 0;
+  CHECK_ARG(comm != nullptr && nccl_unique_id != nullptr, "null argument");
+  CHECK_ARG(nranks >= 1 && rank >= 0 && rank < nranks, "bad nranks / rank (%d / %d)", nranks, rank);
+  if (!nccl().ok) return fail(ATTN_ERR_NCCL, "libnccl.so.2 not loadable");
+  NcclApi::Uid id;
+  memcpy(id.internal, nccl_unique_id, sizeof(id.internal));
+  void* nc = nullptr;
+  attn_status st = nccl_status(nccl().comm_init_rank(&nc, nranks, id, rank), "ncclCommInitRank");
+  if (st != ATTN_OK) return st;
+  *comm = new Comm{nc, nranks, rank};
+  return ATTN_OK;
+}
+
+attn_status attn_nccl_comm_destroy(void* comm) {
+  g_err[0] = 0;
+  if (comm == nullptr) return ATTN_OK;
+  Comm* c = static_cast<Comm*>(comm);
+  attn_status st = nccl().ok ? nccl_status(nccl().comm_destroy(c->nc), "ncclCommDestroy") : ATTN_OK;
+  delete c;
+  return st;
+}
+
+size_t attn_decode_kv_sharded_workspace_bytes(const attn_problem* p, int32_t nranks) {
+  if (p == nullptr || nranks < 1) return 0;
+  const int32_t splits = attn_splitkv_default_splits(p, 0);
+  const size_t rows = (size_t)splits * p->batch * p->heads_q;
+  const size_t packed = (size_t)p->batch * p->heads_q * (p->head_dim + 2);
+  return up256(rows * 4) * 2 + up256(rows * p->head_dim * 4) + up256(packed * 4) * (1 + (size_t)nranks);
+}
+
+attn_status attn_decode_kv_sharded(void* comm, const attn_problem* local, attn_tensor q, attn_tensor k_shard,
+                                   attn_tensor v_shard, void* workspace, size_t workspace_bytes, attn_tensor o,
+                                   float* lse, attn_stream_t stream) {
+  g_err[0] = 0;
+  CHECK_ARG(comm != nullptr && local != nullptr, "null comm / problem");
+  CHECK_ARG(o.ptr != nullptr, "o is NULL");
+  const Comm* c = static_cast<const Comm*>(comm);
+  const size_t need = attn_decode_kv_sharded_workspace_bytes(local, c->nranks);
+  if (workspace == nullptr || workspace_bytes < need)
+    return fail(ATTN_ERR_WORKSPACE_TOO_SMALL, "workspace needs %zu bytes", need);
+  const attn_problem& p = *local;
+  const int32_t splits = attn_splitkv_default_splits(local, 0);
+  const size_t rows = (size_t)splits * p.batch * p.heads_q;
+  const long long bh = (long long)p.batch * p.heads_q, D = p.head_dim, W = D + 2;
+  char* w = static_cast<char*>(workspace);
+  float* pm = reinterpret_cast<float*>(w);
+  float* pl = reinterpret_cast<float*>(w + up256(rows * 4));
+  float* po = reinterpret_cast<float*>(w + 2 * up256(rows * 4));
+  float* send = reinterpret_cast<float*>(w + 2 * up256(rows * 4) + up256(rows * D * 4));
+  float* recv = reinterpret_cast<float*>(reinterpret_cast<char*>(send) + up256(bh * W * 4));
+  // 1. local section over this rank's keys
+  const attn_parts parts{pm, pl, po, splits, bh, p.heads_q, 1, bh * D, (int64_t)p.heads_q * D, D};
+  const attn_tensor none{nullptr, 0, 0, 0};
+  attn_status st = attn_splitkv_decode(local, q, k_shard, v_shard, splits, nullptr, 0, &parts, none, nullptr, stream);
+  if (st != ATTN_OK) return st;
+  int launches = g_launches;
+  // 2. this rank's splits -> one un-normalised triple per (b, hq), packed [B][Hq][D+2]
+  const attn_parts packed{send + D, send + D + 1, send, 1, 0, p.heads_q * W, W, 0, p.heads_q * W, W};
+  st = attn_combine(p.batch, p.heads_q, p.head_dim, &parts, p.dtype, none, nullptr, &packed, stream);
+  if (st != ATTN_OK) return st;
+  launches += g_launches;
+  // 3. all-gather the packed triples
+  st = nccl_status(nccl().all_gather(send, recv, (size_t)bh * W, kNcclFloat32, c->nc,
+                                     reinterpret_cast<cudaStream_t>(stream)), "ncclAllGather");
+  if (st != ATTN_OK) return st;
+  // 4. Eq. 8 over the ranks' triples
+  const attn_parts gathered{recv + D, recv + D + 1, recv, c->nranks, bh * W, p.heads_q * W, W,
+                            bh * W, p.heads_q * W, W};
+  st = attn_combine(p.batch, p.heads_q, p.head_dim, &gathered, p.dtype, o, lse, nullptr, stream);
+  if (st != ATTN_OK) return st;
+  g_launches = launches + g_launches;
+  return ATTN_OK;
 }
 
 }  // extern "C"

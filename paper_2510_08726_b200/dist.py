@@ -118,3 +118,76 @@ def merge_prefill_parts(o_all: torch.Tensor, lse_all: torch.Tensor, out_dtype, f
         return final(o_all, lse_all, out_dtype)
     from . import merge_partials
     return merge_partials(o_all, lse_all, out_dtype=out_dtype, return_lse=True)
+
+
+class NcclComm:
+    """A communicator of the C ABI's own NCCL path (``attn_nccl_comm_init``): the
+    whole KV-sharded decode step -- local section, local merge, all-gather, Eq. 8 --
+    is ONE library call (``attn_decode_kv_sharded``) with no torch on the data path.
+    The 128-byte unique id is created on rank 0 and shipped out of band, here
+    through an existing torch.distributed group (any backend) when given."""
+
+    def __init__(self, rank: int, world: int, unique_id: Optional[bytes] = None, group=None):
+        import ctypes
+        from ._ffi import check, load
+        lib = load()
+        if unique_id is None:
+            buf = ctypes.create_string_buffer(128)
+            if rank == 0:
+                check(lib.attn_nccl_get_unique_id(buf), "attn_nccl_get_unique_id")
+            if world > 1:
+                obj = [buf.raw if rank == 0 else None]
+                dist.broadcast_object_list(obj, src=0, group=group)
+                buf = ctypes.create_string_buffer(obj[0], 128)
+            unique_id = buf.raw
+        self._h = ctypes.c_void_p()
+        check(lib.attn_nccl_comm_init(ctypes.byref(self._h), world, rank, ctypes.create_string_buffer(unique_id, 128)),
+              "attn_nccl_comm_init")
+        self.rank, self.world = rank, world
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes
+        from ._ffi import check, load
+        buf = ctypes.create_string_buffer(128)
+        check(load().attn_nccl_get_unique_id(buf), "attn_nccl_get_unique_id")
+        return buf.raw
+
+    def close(self):
+        from ._ffi import check, load
+        if self._h:
+            check(load().attn_nccl_comm_destroy(self._h), "attn_nccl_comm_destroy")
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def decode_kv_sharded(self, q: torch.Tensor, k_shard: torch.Tensor, v_shard: torch.Tensor, *,
+                          kv_pos_offset: int, seqlen_kv_total: int, out: Optional[torch.Tensor] = None,
+                          return_lse: bool = False, workspace: Optional[torch.Tensor] = None, stream=None,
+                          **variant):
+        """``attn_decode_kv_sharded`` on this communicator (same contract as
+        :func:`decode_kv_sharded`; identical O, lse on every rank)."""
+        import ctypes
+        from . import _as_tensor, _problem, _stream
+        from ._ffi import check, load
+        lib = load()
+        prob = _problem(q, k_shard, scale=variant.get("scale"), causal=variant.get("causal", False),
+                        window=variant.get("window", (-1, -1)), alibi_slopes=variant.get("alibi_slopes"),
+                        softcap=variant.get("softcap", 0.0), q_pos_offset=variant.get("q_pos_offset"),
+                        kv_pos_offset=kv_pos_offset, seqlen_kv_total=seqlen_kv_total)
+        need = lib.attn_decode_kv_sharded_workspace_bytes(ctypes.byref(prob), self.world)
+        if workspace is None or workspace.numel() * workspace.element_size() < need:
+            workspace = torch.empty(need, dtype=torch.uint8, device=q.device)
+        if out is None:
+            out = torch.empty_like(q, memory_format=torch.contiguous_format)
+        lse = torch.empty(q.shape[:2], device=q.device, dtype=torch.float32) if return_lse else None
+        check(lib.attn_decode_kv_sharded(self._h, ctypes.byref(prob), _as_tensor(q), _as_tensor(k_shard),
+                                         _as_tensor(v_shard), workspace.data_ptr(),
+                                         workspace.numel() * workspace.element_size(), _as_tensor(out),
+                                         None if lse is None else lse.data_ptr(), _stream(stream)),
+              "attn_decode_kv_sharded")
+        return (out, lse) if return_lse else out

@@ -137,3 +137,20 @@ def test_product_package_does_not_import_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"\boracle\b", src.replace("oracle/", "")) or "import oracle" not in src, f
                 assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_nccl_entry_points_host_side(lib):
+    """The multi-GPU entry points: NCCL is dlopen'ed at run time (ncclGetUniqueId
+    needs no GPU); argument errors come back as status codes."""
+    buf = ctypes.create_string_buffer(128)
+    assert lib.attn_nccl_get_unique_id(buf) == _ffi.ATTN_OK
+    assert any(buf.raw)
+    assert lib.attn_nccl_get_unique_id(None) == _ffi.ATTN_ERR_INVALID_ARGUMENT
+    assert lib.attn_nccl_comm_destroy(None) == _ffi.ATTN_OK
+    h = ctypes.c_void_p()
+    assert lib.attn_nccl_comm_init(ctypes.byref(h), 2, 2, buf) == _ffi.ATTN_ERR_INVALID_ARGUMENT   # rank >= nranks
+    p = _prob(seqlen_q=1, batch=2, heads_q=32, heads_kv=8, seqlen_kv=16384)
+    ws = lib.attn_decode_kv_sharded_workspace_bytes(ctypes.byref(p), 8)
+    assert ws >= (8 + 1) * 2 * 32 * 130 * 4                # send + nranks receive slots
+    assert lib.attn_decode_kv_sharded(None, ctypes.byref(p), _t(), _t(), _t(), None, 0, _t(), None, None) == \
+        _ffi.ATTN_ERR_INVALID_ARGUMENT

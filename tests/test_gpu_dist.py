@@ -62,6 +62,43 @@ def test_kv_sharded_decode_nccl_one_rank():
             dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("variant", [dict(causal=True), dict(causal=True, alibi=True), dict(softcap=2.0)])
+def test_kv_sharded_decode_c_abi_one_rank(variant):
+    """attn_nccl_comm_init + attn_decode_kv_sharded (the C ABI's own NCCL path, one call
+    for local section + local merge + ncclAllGather + Eq. 8) on a 1-rank communicator;
+    also a shard that is a suffix of a longer sequence (absolute positions)."""
+    variant = dict(variant)
+    B, Hq, Hkv, L, D = 2, 8, 2, 3001, 128
+    alibi = variant.pop("alibi", False)
+    p = problem(B, Hq, Hkv, 1, L, D, alibi_slopes=datagen.alibi_slopes(Hq) if alibi else None, **variant)
+    raw, f64 = gen_qkv(1300, B, Hq, Hkv, 1, L, D)
+    ref_o, ref_l = oracle.attention(p, *f64)
+    q, k, v = (dgd.to_device(x) for x in raw)
+    if alibi:
+        variant["alibi_slopes"] = torch.tensor(datagen.alibi_slopes(Hq), dtype=torch.float32, device="cuda")
+    comm = pdist.NcclComm(0, 1)
+    try:
+        out, lse = comm.decode_kv_sharded(q, k, v, kv_pos_offset=0, seqlen_kv_total=L, return_lse=True, **variant)
+        torch.cuda.synchronize()
+        assert pb.last_launch_count() == 3            # decode + local merge + final combine (+ NCCL)
+        assert_bf16_close(out.float().cpu().numpy().astype(np.float64), ref_o, f"C-ABI kv-sharded {variant}")
+        assert_lse_close(lse.cpu().numpy(), ref_l[:, :, 0], LSE_TOL_BF16, "C-ABI kv-sharded lse")
+        # a shard holding keys [lo, L) of the sequence: the rank's part of the answer
+        lo = 1000
+        ps = problem(B, Hq, Hkv, 1, L - lo, D, seqlen_kv_total=L, q_pos_offset=L - 1, kv_pos_offset=lo,
+                     alibi_slopes=p.alibi_slopes, **variant_no_slopes(variant))
+        ref_s, _ = oracle.attention(ps, f64[0], f64[1][:, :, lo:], f64[2][:, :, lo:])
+        out_s = comm.decode_kv_sharded(q, k[:, :, lo:].contiguous(), v[:, :, lo:].contiguous(), kv_pos_offset=lo,
+                                       seqlen_kv_total=L, **variant)
+        assert_bf16_close(out_s.float().cpu().numpy().astype(np.float64), ref_s, "C-ABI suffix shard")
+    finally:
+        comm.close()
+
+
+def variant_no_slopes(v):
+    return {k: x for k, x in v.items() if k != "alibi_slopes"}
+
+
 # --------------------------------------------------------------------------- context-parallel prefill (NEXT-3)
 @pytest.mark.parametrize("W,variant", [(2, dict(causal=True)), (3, dict(causal=True, window_left=300)),
                                        (4, dict())])
