@@ -214,10 +214,17 @@ def main_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # BENCH_DIST_BACKEND=gloo lets the N > 1 code path run with several ranks sharing one GPU
+    # (a functional check on a 1-GPU box; its timings are meaningless).  Default: NCCL, one GPU per rank.
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     peaks = load_peaks()
     uuid = str(torch.cuda.get_device_properties(dev).uuid)
     gpu_id = uuid if uuid.startswith("GPU-") else f"GPU-{uuid}"  # NVML form
@@ -354,16 +361,57 @@ def main_gpu(args):
                     dstep()
                 dstep = graph.replay
             dms, dclk = timed(dstep, steps, warmup)
+            breakdown = None
+            if world > 1:   # local decode, local combine, all-gather, final combine
+                var5 = dict(causal=True)
+                parts = pdist._local_kernels(qd, kd, vd, kv_pos_offset=lo, seqlen_kv_total=L, num_splits=0,
+                                             variant=var5)
+                send = torch.empty(1, Bd, Hqd, Dd + 2, dtype=torch.float32, device=dev)
+                recv = torch.empty(world, Bd, Hqd, Dd + 2, dtype=torch.float32, device=dev)
+                pieces = {
+                    "local_decode": lambda: pdist._local_kernels(qd, kd, vd, kv_pos_offset=lo, seqlen_kv_total=L,
+                                                                 num_splits=0, variant=var5),
+                    "local_combine": lambda: pdist._merge_kernels(parts, pb.Parts.packed(send)),
+                    "all_gather": lambda: dist.all_gather_into_tensor(recv, send),
+                    "final_combine": lambda: pdist._final_kernels(pb.Parts.packed(recv), torch.bfloat16, False),
+                }
+                breakdown = {key: round(timed(fn, steps, 2, sampler=False)[0], 5) for key, fn in pieces.items()}
+                nl = 0   # kernels of one sharded step: local decode + local combine + final combine
+                for key in ("local_decode", "local_combine", "final_combine"):
+                    pieces[key]()
+                    nl += pb.last_launch_count()
+                del parts, send, recv
             del qd, kd, vd, od, ws
             torch.cuda.empty_cache()
             kv_bytes = 2.0 * Bd * Hkvd * L * Dd * 2
-            return kv_bytes, dms, dclk, nl
+            return kv_bytes, dms, dclk, nl, breakdown
 
-        sweep = {}
+        def run_decode_bh(Bd, steps, warmup):
+            """Communication-free alternative for large B: each rank decodes
+            B/W whole sequences (all L keys), no collective."""
+            Bl = Bd // world
+            qd = torch.empty(Bl, Hqd, 1, Dd, dtype=torch.bfloat16, device=dev)
+            kd = torch.empty(Bl, Hkvd, L, Dd, dtype=torch.bfloat16, device=dev)
+            vd = torch.empty_like(kd)
+            dgd.fill_(qd, seed5, 1, start=rank * qd.numel())
+            dgd.fill_(kd, seed5, 2, start=rank * kd.numel())
+            dgd.fill_(vd, seed5, 3, start=rank * vd.numel())
+            od = torch.empty_like(qd)
+            ws = torch.zeros(pb.workspace_bytes(qd, kd), dtype=torch.uint8, device=dev)
+            fn = lambda: pb.splitkv_decode(qd, kd, vd, causal=True, out=od, workspace=ws)  # noqa: E731
+            fn()
+            ms, _ = timed(fn, steps, warmup, sampler=False)
+            del qd, kd, vd, od, ws
+            torch.cuda.empty_cache()
+            return 2.0 * Bd * Hkvd * L * Dd * 2 / (ms * 1e-3) / 1e9, ms
+
+        sweep, breakdowns = {}, {}
         for Bd in sorted(set([1, 4, args.decode_batch])):
-            kv_bytes, dms, dclk, dl = run_decode(Bd, max(args.steps, 20), args.warmup)
+            kv_bytes, dms, dclk, dl, bd = run_decode(Bd, max(args.steps, 20), args.warmup)
             sweep[Bd] = {"GB/s": kv_bytes / (dms * 1e-3) / 1e9, "ms_per_step": dms,
                          "frac_of_hbm_peak": kv_bytes / world / (dms * 1e-3) / 1e9 / peaks["hbm"]}
+            if bd is not None:
+                breakdowns[str(Bd)] = bd
         Bd = args.decode_batch
         gbs, dms = sweep[Bd]["GB/s"], sweep[Bd]["ms_per_step"]
         per_rank = gbs / world
@@ -377,11 +425,18 @@ def main_gpu(args):
                        "launch": "CUDA graph replay" if world == 1 and not args.no_graph else "eager"},
             "batch_sweep": {str(b): {k: round(v, 4) for k, v in d.items()} for b, d in sweep.items()},
             "gpu_launches_per_step": dl,
+            "breakdown_ms": breakdowns or None,
             "roofline": {"bound": "hbm", "achieved": per_rank, "peak": peaks["hbm"], "unit": "GB/s",
                          "frac": per_rank / peaks["hbm"], "traffic": traffic_decode,
                          "peak_src": f"{peaks['src']} hbm_gbs (copy)", "kernel": "decode_split_kernel (fused Eq. 8 combine)",
                          "algorithmic_bytes_per_launch": 2.0 * Bd * Hkvd * L * Dd * 2 / world},
         }
+
+        if world > 1 and args.decode_batch % world == 0:
+            gbs_bh, ms_bh = run_decode_bh(args.decode_batch, max(args.steps, 20), args.warmup)
+            line["decode"]["bh_sharded"] = {
+                "GB/s": gbs_bh, "ms_per_step": ms_bh, "scaling": "strong",
+                "parallelism": f"(b, hkv) sharding: {args.decode_batch // world} sequences per rank, no collective"}
 
     # ------------------------------------------------------------- NEXT-4: Fig. 2 reduction chain (softmax rows)
     if not args.no_softmax:
