@@ -138,6 +138,33 @@ ATTN_API attn_status attn_fused_fwd(const attn_problem* prob, attn_tensor q, att
                            attn_tensor o, float* lse, attn_stream_t stream);
 
 /* ---------------------------------------------------------------------
+ * Rolling Update with the KV axis also split across CTAs (NEXT-2: small
+ * grids such as chunked prefill / multi-token decode, s_q << s_kv, where
+ * B * Hq * ceil(s_q / 256) CTAs would leave most SMs idle).  Split s runs the
+ * same rolling loop over a contiguous run of 128-key tiles and writes a
+ * NORMALISED partial (O_s, lse_s) -- the repaired triple (m = lse_s, l = 1,
+ * O_s) of Thm. 2 -- into the workspace; Eq. 8 then merges the
+ * splits into o / lse.  Exact in real arithmetic for any split (Eq. 4); the
+ * partial O is rounded to q's dtype once before the merge.
+ *
+ * attn_fused_fwd_default_splits: min(sm_count / units, n_kv_tiles / 4, 16)
+ *   with units = B * Hq * ceil(s_q / 256) and 128-key tiles, or 1 when that is
+ *   below 4 (a split pays for its merge launch only then -- measured).  Always
+ *   1 for fp32.
+ * attn_fused_fwd_workspace_bytes: DEVICE workspace (256-byte aligned) for
+ *   num_splits (0 = default); 0 when no split is used.
+ * attn_fused_fwd_splitkv: num_splits 0 = default, 1 = attn_fused_fwd.  Two
+ *   launches when split (prefill kernel + merge).  Errors: those of
+ *   attn_fused_fwd, WORKSPACE_TOO_SMALL, ALIGNMENT (workspace), UNSUPPORTED
+ *   (fp32 with num_splits > 1).
+ * ------------------------------------------------------------------- */
+ATTN_API int32_t attn_fused_fwd_default_splits(const attn_problem* prob, int32_t sm_count);
+ATTN_API size_t attn_fused_fwd_workspace_bytes(const attn_problem* prob, int32_t num_splits);
+ATTN_API attn_status attn_fused_fwd_splitkv(const attn_problem* prob, attn_tensor q, attn_tensor k, attn_tensor v,
+                                            attn_tensor o, float* lse, int32_t num_splits, void* workspace,
+                                            size_t workspace_bytes, attn_stream_t stream);
+
+/* ---------------------------------------------------------------------
  * Split-K Update decode (Alg. 2, Fig. 5): seqlen_q must be 1, dtype bf16 or fp16,
  * D in {64, 128}.  The KV axis of every (b, hkv) is cut into num_splits
  * contiguous parts (PrivatizeReduce); each CTA streams its part

@@ -70,12 +70,14 @@ def fused_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: Optio
               alibi_slopes: Optional[torch.Tensor] = None, softcap: float = 0.0,
               q_pos_offset: Optional[int] = None, kv_pos_offset: int = 0,
               seqlen_kv_total: Optional[int] = None, out: Optional[torch.Tensor] = None,
-              lse: Optional[torch.Tensor] = None, return_lse: bool = False, stream=None):
-    """Rolling Update forward (``attn_fused_fwd``).
+              lse: Optional[torch.Tensor] = None, return_lse: bool = False, kv_splits: int = 0, stream=None):
+    """Rolling Update forward (``attn_fused_fwd`` / ``attn_fused_fwd_splitkv``).
 
     Device tensors run in place on ``stream``.  Host (CPU) tensors take the
     end-to-end path: copied to the current device, computed, copied back
-    (pinned host memory makes the copies asynchronous)."""
+    (pinned host memory makes the copies asynchronous).  ``kv_splits``: 0 lets
+    the library split the KV axis across CTAs for small grids (NEXT-2), 1 never
+    splits, n > 1 forces n splits."""
     lib = load()
     if q.device.type == "cpu":
         dev = torch.device("cuda", torch.cuda.current_device())
@@ -96,9 +98,32 @@ def fused_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: Optio
         lse = torch.empty(q.shape[:3], device=q.device, dtype=torch.float32)
     if lse is not None and (not lse.is_contiguous() or lse.dtype != torch.float32):
         raise ValueError("lse must be a contiguous float32 [B, Hq, Sq] tensor")
-    check(lib.attn_fused_fwd(ctypes.byref(prob), _as_tensor(q), _as_tensor(k), _as_tensor(v), _as_tensor(out),
-                             None if lse is None else lse.data_ptr(), _stream(stream)), "attn_fused_fwd")
+    splits = kv_splits if kv_splits > 0 else lib.attn_fused_fwd_default_splits(ctypes.byref(prob), 0)
+    if splits <= 1:
+        check(lib.attn_fused_fwd(ctypes.byref(prob), _as_tensor(q), _as_tensor(k), _as_tensor(v), _as_tensor(out),
+                                 None if lse is None else lse.data_ptr(), _stream(stream)), "attn_fused_fwd")
+    else:
+        need = lib.attn_fused_fwd_workspace_bytes(ctypes.byref(prob), splits)
+        ws = _scratch(q.device, need, stream)
+        check(lib.attn_fused_fwd_splitkv(ctypes.byref(prob), _as_tensor(q), _as_tensor(k), _as_tensor(v),
+                                         _as_tensor(out), None if lse is None else lse.data_ptr(), splits,
+                                         ws.data_ptr(), ws.numel(), _stream(stream)), "attn_fused_fwd_splitkv")
     return (out, lse) if return_lse else out
+
+
+_SCRATCH = {}
+
+
+def _scratch(device, need: int, stream) -> torch.Tensor:
+    """Per-(device, stream) scratch for the split-KV prefill partials (no zeroing needed)."""
+    key = (device.index if device.index is not None else torch.cuda.current_device(), _stream(stream).value)
+    ws = _SCRATCH.get(key)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(max(need, 1 << 20), dtype=torch.uint8, device=device)
+        if stream is not None:
+            stream.wait_stream(torch.cuda.current_stream(device))
+        _SCRATCH[key] = ws
+    return ws
 
 
 class Parts:

@@ -25,7 +25,8 @@ EXPORTED = ("attn_fused_fwd", "attn_splitkv_default_splits", "attn_splitkv_works
             "attn_splitkv_decode", "attn_combine", "attn_status_string", "attn_last_error",
             "attn_abi_version", "attn_last_launch_count", "attn_merge_partials", "attn_softmax_rows",
             "attn_nccl_get_unique_id", "attn_nccl_comm_init", "attn_nccl_comm_destroy",
-            "attn_decode_kv_sharded_workspace_bytes", "attn_decode_kv_sharded")
+            "attn_decode_kv_sharded_workspace_bytes", "attn_decode_kv_sharded",
+            "attn_fused_fwd_default_splits", "attn_fused_fwd_workspace_bytes", "attn_fused_fwd_splitkv")
 
 
 class AttnTensor(ctypes.Structure):
@@ -65,6 +66,12 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     vp, i32, f32p = ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p
     lib.attn_fused_fwd.argtypes = [P, T, T, T, T, f32p, vp]
     lib.attn_fused_fwd.restype = ctypes.c_int
+    lib.attn_fused_fwd_default_splits.argtypes = [P, i32]
+    lib.attn_fused_fwd_default_splits.restype = i32
+    lib.attn_fused_fwd_workspace_bytes.argtypes = [P, i32]
+    lib.attn_fused_fwd_workspace_bytes.restype = ctypes.c_size_t
+    lib.attn_fused_fwd_splitkv.argtypes = [P, T, T, T, T, f32p, i32, vp, ctypes.c_size_t, vp]
+    lib.attn_fused_fwd_splitkv.restype = ctypes.c_int
     lib.attn_splitkv_default_splits.argtypes = [P, i32]
     lib.attn_splitkv_default_splits.restype = i32
     lib.attn_splitkv_workspace_bytes.argtypes = [P, i32]

@@ -161,11 +161,42 @@ const char* attn_status_string(attn_status s) {
 
 attn_status attn_fused_fwd(const attn_problem* prob, attn_tensor q, attn_tensor k, attn_tensor v, attn_tensor o,
                            float* lse, attn_stream_t stream) {
+  return attn_fused_fwd_splitkv(prob, q, k, v, o, lse, 1, nullptr, 0, stream);
+}
+
+int32_t attn_fused_fwd_default_splits(const attn_problem* p, int32_t sm_count) {
+  if (p == nullptr || p->dtype == ATTN_FP32 || p->batch < 1 || p->heads_q < 1 || p->seqlen_q < 1) return 1;
+  if (sm_count <= 0) sm_count = sm_count_cached();
+  const int64_t units = (int64_t)p->batch * p->heads_q * ((p->seqlen_q + 255) / 256);
+  const int64_t ntiles = (p->seqlen_kv + 127) / 128;
+  // Measured on the Table 3 grid (tools/sweep.py --table3): a split pays for its merge
+  // launch only with >= 4 splits of >= 4 KV tiles each (s_kv >= 2048 at s_q <= 256:
+  // 28.7 -> 20.8 us); fewer / shorter splits were slower than the plain kernel.
+  int64_t splits = sm_count / units;
+  if (splits > ntiles / 4) splits = ntiles / 4;
+  if (splits > 16) splits = 16;
+  return splits < 4 ? 1 : (int32_t)splits;
+}
+
+size_t attn_fused_fwd_workspace_bytes(const attn_problem* p, int32_t num_splits) {
+  if (p == nullptr) return 0;
+  if (num_splits <= 0) num_splits = attn_fused_fwd_default_splits(p, 0);
+  if (num_splits <= 1) return 0;
+  const size_t rows = (size_t)num_splits * p->batch * p->heads_q * p->seqlen_q;
+  auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
+  return up(rows * p->head_dim * 2) + up(rows * 4);   // partial O (q's dtype), partial lse (fp32)
+}
+
+attn_status attn_fused_fwd_splitkv(const attn_problem* prob, attn_tensor q, attn_tensor k, attn_tensor v,
+                                   attn_tensor o, float* lse, int32_t num_splits, void* workspace,
+                                   size_t workspace_bytes, attn_stream_t stream) {
   g_err[0] = 0;
   attn::VariantParams vp;
   attn_status st = check_problem(prob, &vp);
   if (st != ATTN_OK) return st;
   const attn_problem& p = *prob;
+  if (num_splits < 0) return fail(ATTN_ERR_INVALID_ARGUMENT, "num_splits must be >= 0");
+  if (num_splits == 0) num_splits = attn_fused_fwd_default_splits(prob, 0);
   const int eb = p.dtype == ATTN_FP32 ? 4 : 2;
   if ((st = check_tensor(q, "q", eb, p.batch, p.heads_q, p.seqlen_q)) != ATTN_OK) return st;
   if ((st = check_tensor(k, "k", eb, p.batch, p.heads_kv, p.seqlen_kv)) != ATTN_OK) return st;
@@ -184,24 +215,68 @@ attn_status attn_fused_fwd(const attn_problem* prob, attn_tensor q, attn_tensor 
     if ((st = make_map(&a.tm_q, q, p.batch, p.heads_q, p.seqlen_q, p.head_dim, 64, 128, true, a.f16)) != ATTN_OK) return st;
     if ((st = make_map(&a.tm_k, k, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, 128, true, a.f16)) != ATTN_OK) return st;
     if ((st = make_map(&a.tm_v, v, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, 128, true, a.f16)) != ATTN_OK) return st;
-    if ((st = make_map(&a.tm_o, o, p.batch, p.heads_q, p.seqlen_q, p.head_dim, 64, 128, true, a.f16)) != ATTN_OK) return st;
-    st = cuda_status(attn::launch_fwd_tc(a, s, &launches), "fwd_tc launch");
-  } else {
-    if (p.head_dim > 256) return fail(ATTN_ERR_UNSUPPORTED, "fp32 head_dim must be <= 256");
-    attn::FwdSimtArgs a;
-    a.s = shape_of(prob);
-    a.v = vp;
-    a.q = static_cast<const float*>(q.ptr);
-    a.k = static_cast<const float*>(k.ptr);
-    a.v_ = static_cast<const float*>(v.ptr);
-    a.o = static_cast<float*>(o.ptr);
-    a.q_sb = q.stride_b; a.q_sh = q.stride_h; a.q_ss = q.stride_s;
-    a.k_sb = k.stride_b; a.k_sh = k.stride_h; a.k_ss = k.stride_s;
-    a.v_sb = v.stride_b; a.v_sh = v.stride_h; a.v_ss = v.stride_s;
-    a.o_sb = o.stride_b; a.o_sh = o.stride_h; a.o_ss = o.stride_s;
-    a.lse = lse;
-    st = cuda_status(attn::launch_fwd_simt(a, s, &launches), "fwd_simt launch");
+    if (num_splits <= 1) {
+      if ((st = make_map(&a.tm_o, o, p.batch, p.heads_q, p.seqlen_q, p.head_dim, 64, 128, true, a.f16)) != ATTN_OK) return st;
+      return (st = cuda_status(attn::launch_fwd_tc(a, s, &launches), "fwd_tc launch")) == ATTN_OK
+                 ? (g_launches = launches, ATTN_OK) : st;
+    }
+    // KV split: partial (O_s, lse_s) per split into the workspace, then Eq. 8 over the splits
+    const size_t need = attn_fused_fwd_workspace_bytes(prob, num_splits);
+    if (workspace == nullptr || workspace_bytes < need)
+      return fail(ATTN_ERR_WORKSPACE_TOO_SMALL, "workspace needs %zu bytes", need);
+    if ((reinterpret_cast<uintptr_t>(workspace) & 255) != 0)
+      return fail(ATTN_ERR_ALIGNMENT, "workspace must be 256-byte aligned");
+    const long long rows = (long long)p.batch * p.heads_q * p.seqlen_q;
+    const size_t obytes = (((size_t)num_splits * rows * p.head_dim * 2) + 255) & ~size_t(255);
+    void* po = workspace;
+    float* plse = reinterpret_cast<float*>(static_cast<char*>(workspace) + obytes);
+    const int ntiles = (p.seqlen_kv + 127) / 128;
+    a.s.kv_splits = num_splits;
+    a.s.kv_split_tiles = (ntiles + num_splits - 1) / num_splits;
+    a.lse = plse;
+    const attn_tensor pt{po, (int64_t)p.heads_q * p.seqlen_q * p.head_dim, (int64_t)p.seqlen_q * p.head_dim,
+                         p.head_dim};
+    if ((st = make_map(&a.tm_o, pt, num_splits * p.batch, p.heads_q, p.seqlen_q, p.head_dim, 64, 128, true, a.f16)) !=
+        ATTN_OK)
+      return st;
+    if ((st = cuda_status(attn::launch_fwd_tc(a, s, &launches), "fwd_tc launch")) != ATTN_OK) return st;
+    attn::MergeArgs m{};
+    m.P = num_splits;
+    m.D = p.head_dim;
+    m.rows = rows;
+    m.in_dtype = p.dtype;
+    m.out_dtype = p.dtype;
+    m.o_in = po;
+    m.o_sp = rows * p.head_dim;
+    m.o_sr = p.head_dim;
+    m.lse_in = plse;
+    m.l_sp = rows;
+    m.o_out = o.ptr;
+    m.o_out_sr = o.stride_s;
+    m.out_H = p.heads_q;
+    m.out_Sq = p.seqlen_q;
+    m.o_out_sb = o.stride_b;
+    m.o_out_sh = o.stride_h;
+    m.lse_out = lse;
+    if ((st = cuda_status(attn::launch_merge(m, s, &launches), "merge launch")) != ATTN_OK) return st;
+    g_launches = launches;
+    return ATTN_OK;
   }
+  if (num_splits > 1) return fail(ATTN_ERR_UNSUPPORTED, "the fp32 path has no KV split");
+  if (p.head_dim > 256) return fail(ATTN_ERR_UNSUPPORTED, "fp32 head_dim must be <= 256");
+  attn::FwdSimtArgs a;
+  a.s = shape_of(prob);
+  a.v = vp;
+  a.q = static_cast<const float*>(q.ptr);
+  a.k = static_cast<const float*>(k.ptr);
+  a.v_ = static_cast<const float*>(v.ptr);
+  a.o = static_cast<float*>(o.ptr);
+  a.q_sb = q.stride_b; a.q_sh = q.stride_h; a.q_ss = q.stride_s;
+  a.k_sb = k.stride_b; a.k_sh = k.stride_h; a.k_ss = k.stride_s;
+  a.v_sb = v.stride_b; a.v_sh = v.stride_h; a.v_ss = v.stride_s;
+  a.o_sb = o.stride_b; a.o_sh = o.stride_h; a.o_ss = o.stride_s;
+  a.lse = lse;
+  st = cuda_status(attn::launch_fwd_simt(a, s, &launches), "fwd_simt launch");
   if (st == ATTN_OK) g_launches = launches;
   return st;
 }

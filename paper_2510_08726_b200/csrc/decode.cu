@@ -439,7 +439,13 @@ __global__ void __launch_bounds__(128) merge_kernel(const MergeArgs a) {
 #pragma unroll
     for (int r = 0; r < kMaxDL; ++r) {
       const int d = lane + 32 * r;
-      if (d < a.D) store_elem(a.o_out, row * a.o_out_sr + d, a.out_dtype, acc[r] * inv);
+      if (d >= a.D) continue;
+      long long oi = row * a.o_out_sr + d;
+      if (a.out_Sq > 0) {
+        const long long bh = row / a.out_Sq, i = row % a.out_Sq;
+        oi = (bh / a.out_H) * a.o_out_sb + (bh % a.out_H) * a.o_out_sh + i * a.o_out_sr + d;
+      }
+      store_elem(a.o_out, oi, a.out_dtype, acc[r] * inv);
     }
   }
   if (a.lse_out && lane == 0) a.lse_out[row] = L > 0.f ? M + logf(L) : -INFINITY;
@@ -449,7 +455,7 @@ template <int D, bool kAlibi, bool kSoftcap, bool kF16>
 cudaError_t launch_dec_t(const DecodeArgs& a, cudaStream_t stream) {
   using C = DCfg<D>;
   auto kern = decode_split_kernel<D, kAlibi, kSoftcap, kF16>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+  cudaError_t e = set_smem_once<decode_split_kernel<D, kAlibi, kSoftcap, kF16>>(C::kSmemBytes);
   if (e != cudaSuccess) return e;
   dim3 grid(a.num_splits, a.s.Hkv, a.s.B);
   kern<<<grid, kThreads, C::kSmemBytes, stream>>>(a.tm_k, a.tm_v, a);

@@ -264,10 +264,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int qblk = v.causal ? (int)(gridDim.x - 1 - blockIdx.x) : (int)blockIdx.x;  // heavy causal tiles first
-  const int hq = blockIdx.y, b = blockIdx.z;
+  const int hq = blockIdx.y;
+  const int zb = blockIdx.z;                                 // output batch index (split * B + b)
+  const int b = s.kv_splits > 1 ? zb % s.B : zb;              // input batch index
   const int hkv = hq / (s.Hq / s.Hkv);                       // R6: contiguous GQA groups
   const int row0 = qblk * 2 * BM;
-  const Range rng0 = tile_range(s, v, row0), rng1 = tile_range(s, v, row0 + BM);
+  Range rng0 = tile_range(s, v, row0), rng1 = tile_range(s, v, row0 + BM);
+  if (s.kv_splits > 1) {   // this CTA's KV split: a contiguous run of whole tiles
+    const int t_lo = (zb / s.B) * s.kv_split_tiles, t_hi = t_lo + s.kv_split_tiles;
+    for (Range* r : {&rng0, &rng1}) {
+      r->lo = max(r->lo, t_lo);
+      r->hi = min(r->hi, t_hi);
+      if (r->lo >= r->hi) r->lo = r->hi = 0;
+    }
+  }
   const bool has_rows1 = row0 + BM < s.Sq;
   int ulo = 0, uhi = 0;
   if (rng0.hi > rng0.lo && rng1.hi > rng1.lo) {
@@ -721,12 +731,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       fence_proxy_async_smem();
       named_bar_sync(1 + t, kTileThreads);
       if (tid_t == 0) {
-        for (int bx = 0; bx < C::kBoxes; ++bx) tma_store_4d(&tm_o, sOut + bx * BM * 128, bx * 64, row0 + t * BM, hq, b);
+        for (int bx = 0; bx < C::kBoxes; ++bx) tma_store_4d(&tm_o, sOut + bx * BM * 128, bx * 64, row0 + t * BM, hq, zb);
         bulk_commit();
         bulk_wait_read0();
       }
       if (lse != nullptr && i < s.Sq && half == 0)
-        lse[((size_t)b * s.Hq + hq) * s.Sq + i] = l > 0.f ? m_ref * kLn2 + logf(l) : -INFINITY;
+        lse[((size_t)zb * s.Hq + hq) * s.Sq + i] = l > 0.f ? m_ref * kLn2 + logf(l) : -INFINITY;
     }
   }
 
@@ -747,9 +757,9 @@ template <int D, bool kAlibi, bool kSoftcap, bool kF16>
 cudaError_t launch_t(const FwdTcArgs& a, cudaStream_t stream) {
   using C = Cfg<D>;
   auto kern = fwd_tc_kernel<D, kAlibi, kSoftcap, kF16>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+  cudaError_t e = set_smem_once<fwd_tc_kernel<D, kAlibi, kSoftcap, kF16>>(C::kSmemBytes);
   if (e != cudaSuccess) return e;
-  dim3 grid((a.s.Sq + 2 * BM - 1) / (2 * BM), a.s.Hq, a.s.B);
+  dim3 grid((a.s.Sq + 2 * BM - 1) / (2 * BM), a.s.Hq, a.s.B * (a.s.kv_splits > 1 ? a.s.kv_splits : 1));
   kern<<<grid, kThreads, C::kSmemBytes, stream>>>(a.tm_q, a.tm_k, a.tm_v, a.tm_o, a.s, a.v, a.lse);
   return cudaGetLastError();
 }

@@ -1,11 +1,26 @@
 // kernels.h -- internal (non-ABI) launch interface between the host layer
 // (api.cu) and the kernels.  Not installed; no torch types anywhere.
 #pragma once
+#include <atomic>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 namespace attn {
+
+// cudaFuncSetAttribute(max dynamic smem) once per (kernel, device): it costs
+// ~1 us of host time per launch otherwise (visible on small, launch-bound shapes).
+template <auto kKern>
+inline cudaError_t set_smem_once(int bytes) {
+  static std::atomic<unsigned long long> done{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_relaxed) & bit) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kKern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit);
+  return e;
+}
 
 // Variant parameters shared by all kernels, pre-converted on the host to the
 // log2 domain the kernels compute in (exp(x) = exp2(x * log2 e)).
@@ -24,6 +39,10 @@ struct VariantParams {
 
 struct Shape {
   int B, Hq, Hkv, Sq, Skv, D;
+  // Prefill KV split (NEXT-2, small grids): kv_splits CTAs per (q-block, hq, b), split s
+  // owning KV tiles [s*kv_split_tiles, (s+1)*kv_split_tiles); outputs go to batch index
+  // s*B + b of a partial [kv_splits*B] output.  kv_splits <= 1: off.
+  int kv_splits = 1, kv_split_tiles = 0;
 };
 
 // ------------------------------------------------------------ tcgen05 prefill
@@ -92,6 +111,9 @@ struct MergeArgs {
   const float* lse_in; long long l_sp;
   void* o_out; long long o_out_sr;
   float* lse_out;
+  // out_Sq > 0: row r = (b * out_H + h) * out_Sq + i is written at
+  // o_out + b*o_out_sb + h*o_out_sh + i*o_out_sr (a strided [B][H][Sq][D] output)
+  int out_H = 0, out_Sq = 0; long long o_out_sb = 0, o_out_sh = 0;
 };
 cudaError_t launch_merge(const MergeArgs& a, cudaStream_t stream, int* launches);
 

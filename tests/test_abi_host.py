@@ -154,3 +154,20 @@ def test_nccl_entry_points_host_side(lib):
     assert ws >= (8 + 1) * 2 * 32 * 130 * 4                # send + nranks receive slots
     assert lib.attn_decode_kv_sharded(None, ctypes.byref(p), _t(), _t(), _t(), None, 0, _t(), None, None) == \
         _ffi.ATTN_ERR_INVALID_ARGUMENT
+
+
+def test_prefill_split_heuristic_is_host_only(lib):
+    """attn_fused_fwd_default_splits / _workspace_bytes (NEXT-2) are pure host functions."""
+    big = _prob(batch=8, heads_q=16, heads_kv=16, seqlen_q=4096, seqlen_kv=4096)
+    assert lib.attn_fused_fwd_default_splits(ctypes.byref(big), 148) == 1       # grid fills the GPU
+    assert lib.attn_fused_fwd_workspace_bytes(ctypes.byref(big), 0) == 0
+    small = _prob(batch=1, heads_q=32, heads_kv=32, seqlen_q=16, seqlen_kv=2048)
+    assert lib.attn_fused_fwd_default_splits(ctypes.byref(small), 148) == 4     # 32 units -> 4 per unit
+    ws = lib.attn_fused_fwd_workspace_bytes(ctypes.byref(small), 4)
+    assert ws >= 4 * 32 * 16 * (128 * 2 + 4)
+    short = _prob(batch=1, heads_q=2, heads_kv=2, seqlen_q=16, seqlen_kv=1024)
+    assert lib.attn_fused_fwd_default_splits(ctypes.byref(short), 148) == 1     # 8 tiles: < 4 splits of 4
+    wide = _prob(batch=1, heads_q=64, heads_kv=8, seqlen_q=512, seqlen_kv=8192)
+    assert lib.attn_fused_fwd_default_splits(ctypes.byref(wide), 148) == 1      # 128 units: < 4 per unit
+    f32 = _prob(batch=1, heads_q=2, heads_kv=2, seqlen_q=16, seqlen_kv=4096, dtype=_ffi.ATTN_FP32)
+    assert lib.attn_fused_fwd_default_splits(ctypes.byref(f32), 148) == 1

@@ -129,6 +129,59 @@ def test_bf16_prefill_rectangular(Sq, Skv, extra):
     assert_lse_close(lse.cpu().numpy(), ref_l, LSE_TOL_BF16, "lse")
 
 
+SPLIT_CASES = [   # (B, Hq, Hkv, Sq, Skv, D, splits, variant)
+    (1, 4, 2, 16, 2048, 128, 4, dict()),                                   # Table 3 corner, GQA
+    (1, 2, 2, 100, 1000, 128, 3, dict(causal=True)),                       # chunked prefill, ragged
+    (2, 2, 1, 300, 1300, 64, 5, dict(causal=True, alibi=True)),            # 2 q-blocks, D = 64
+    (1, 2, 2, 64, 777, 128, 6, dict(softcap=2.0)),
+    (1, 2, 1, 200, 1500, 128, 4, dict(window_left=300, window_right=0, causal=True)),   # empty splits
+    (1, 2, 2, 129, 900, 128, 7, dict(causal=True, kv_pos_offset=100, seqlen_kv_total=1000)),
+]
+
+
+@pytest.mark.parametrize("case", range(len(SPLIT_CASES)))
+def test_prefill_kv_split(case):
+    """NEXT-2: the KV axis split across CTAs (normalised partials + Eq. 8 merge) equals the
+    oracle, and the unsplit kernel within tolerance; 2 launches."""
+    B, Hq, Hkv, Sq, Skv, D, splits, var = SPLIT_CASES[case]
+    var = dict(var)
+    if var.pop("alibi", False):
+        var["alibi_slopes"] = datagen.alibi_slopes(Hq)
+    p = problem(B, Hq, Hkv, Sq, Skv, D, **var)
+    raw, f64 = gen_qkv(1500 + case, B, Hq, Hkv, Sq, Skv, D)
+    ref_o, ref_l = oracle.attention(p, *f64)
+    q, k, v = (dgd.to_device(x) for x in raw)
+    o, lse = pb.fused_fwd(q, k, v, return_lse=True, kv_splits=splits, **_kw_from(p))
+    torch.cuda.synchronize()
+    assert pb.last_launch_count() == 2
+    assert_bf16_close(_bf16_np(o), ref_o, f"split case {case}")
+    assert_lse_close(lse.cpu().numpy(), ref_l, LSE_TOL_BF16, f"split case {case} lse")
+    o1 = pb.fused_fwd(q, k, v, kv_splits=1, **_kw_from(p))
+    torch.cuda.synchronize()
+    assert pb.last_launch_count() == 1
+    assert (o1.float() - o.float()).abs().max().item() <= 2e-2
+    # strided output view (the merge writes a [B][H][Sq][D] view with arbitrary strides)
+    big = torch.zeros(B, Hq, Sq + 3, D + 64, dtype=q.dtype, device="cuda")
+    pb.fused_fwd(q, k, v, out=big[:, :, 1:Sq + 1, 32:32 + D], kv_splits=splits, **_kw_from(p))
+    torch.cuda.synchronize()
+    assert torch.equal(big[:, :, 1:Sq + 1, 32:32 + D], o)
+    assert big[:, :, 0].abs().max().item() == 0 and big[..., :32].abs().max().item() == 0
+
+
+def test_prefill_kv_split_fp16_auto():
+    """Auto split on a small grid (B*Hq*qblocks << SMs), fp16."""
+    B, Hq, Hkv, Sq, Skv, D = 1, 8, 8, 32, 2048, 128
+    p = problem(B, Hq, Hkv, Sq, Skv, D, causal=True)
+    raw, f64 = gen_qkv(1600, B, Hq, Hkv, Sq, Skv, D, dtype="f16")
+    ref_o, _ = oracle.attention(p, *f64)
+    q, k, v = (dgd.to_device(x, dtype="f16") for x in raw)
+    o = pb.fused_fwd(q, k, v, **_kw_from(p))
+    torch.cuda.synchronize()
+    assert pb.last_launch_count() == 2          # the default split kicked in
+    assert o.dtype == torch.float16
+    assert_bf16_close(_bf16_np(o), ref_o, "fp16 auto split")
+
+
 def test_bf16_prefill_strided_views_and_determinism():
     """Non-contiguous (sliced) q/k/v views and bitwise run-to-run determinism."""
     B, Hq, Hkv, S, D = 2, 4, 4, 300, 128

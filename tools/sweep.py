@@ -73,6 +73,20 @@ def time_fn(fn, reps, warmup=3):
     return s0.elapsed_time(s1) / reps
 
 
+def time_graph(fn, reps):
+    """Same step captured in a CUDA graph and replayed: the GPU time without the
+    Python binding's per-call host cost (which dominates launch-bound shapes)."""
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        fn()
+    torch.cuda.current_stream().wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    return time_fn(g.replay, reps)
+
+
 def run_op(name, seq, B, dtype, reps):
     mode, arch, Hq, Hkv, D, var = OPERATORS[name]
     tdt = torch.float16 if dtype == "fp16" else torch.bfloat16
@@ -87,7 +101,7 @@ def run_op(name, seq, B, dtype, reps):
     if mode == "PF":
         fn = lambda: pb.fused_fwd(q, k, v, out=out, **kw)  # noqa: E731
     else:
-        ws = torch.empty(pb.workspace_bytes(q, k), dtype=torch.uint8, device="cuda")
+        ws = torch.zeros(pb.workspace_bytes(q, k), dtype=torch.uint8, device="cuda")   # ticket block starts at 0
         fn = lambda: pb.splitkv_decode(q, k, v, out=out, workspace=ws, **kw)  # noqa: E731
     ms = time_fn(fn, reps)
     flops = 4.0 * D * pairs(Sq, seq, var) * B * Hq
@@ -96,13 +110,40 @@ def run_op(name, seq, B, dtype, reps):
             "ms": ms, "TFLOP/s": flops / (ms * 1e-3) / 1e12, "KV GB/s": kv_bytes / (ms * 1e-3) / 1e9}
 
 
+def run_table3(reps, dtype):
+    """Table 3's grid: global (non-causal) attention, s_q <= s_kv,
+    s_q in 16..2048, s_kv in 128..2048 (chunked prefill / multi-token shapes, NEXT-2).
+    The paper gives no head shape for it: B = 1, 32 heads, D = 128 (reading R15)."""
+    tdt = torch.float16 if dtype == "fp16" else torch.bfloat16
+    out = []
+    for skv in (128, 256, 512, 1024, 2048):
+        for sq in (16, 32, 64, 128, 256, 512, 1024, 2048):
+            if sq > skv:
+                continue
+            q = dgd.tensor(8, 1, (1, 32, sq, 128), tdt)
+            k = dgd.tensor(8, 2, (1, 32, skv, 128), tdt)
+            v = dgd.tensor(8, 3, (1, 32, skv, 128), tdt)
+            o = torch.empty_like(q)
+            fn = lambda: pb.fused_fwd(q, k, v, out=o)  # noqa: E731
+            ms = time_fn(fn, reps)
+            msg = time_graph(fn, reps)
+            flops = 4.0 * 128 * sq * skv * 32
+            out.append({"s_q": sq, "s_kv": skv, "us": ms * 1e3, "TFLOP/s": flops / (ms * 1e-3) / 1e12,
+                        "us_graph": msg * 1e3, "TFLOP/s_graph": flops / (msg * 1e-3) / 1e12})
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--dtype", default="fp16", choices=["fp16", "bf16"])
     ap.add_argument("--reps", type=int, default=15)
     ap.add_argument("--max-log2", type=int, default=15)
     ap.add_argument("--ops", default="all")
+    ap.add_argument("--table3", action="store_true", help="only the s_q x s_kv grid of Table 3")
     args = ap.parse_args()
+    if args.table3:
+        print(json.dumps({"dtype": args.dtype, "table3": run_table3(args.reps, args.dtype)}, indent=1))
+        return
     ops = list(OPERATORS) if args.ops == "all" else [o for o in OPERATORS if o.split()[0] in args.ops.split(",")]
     res = {"dtype": args.dtype, "protocol": f"mean of {args.reps} runs after 3 warm-ups, CUDA events, no L2 flush "
            "(the paper's protocol P:1006-1011)", "operators": [], "batch_scaling": []}
