@@ -31,6 +31,8 @@
 //   tag-updates to any reference (Eq. 6).
 #include <math.h>
 
+#include <algorithm>
+
 #include "kernels.h"
 #include "ptx.cuh"
 
@@ -75,6 +77,11 @@ constexpr uint32_t kBarS0 = 9;                    // 9 / 10: "S_t loaded into re
 // serialises softmax -> PV -> QK -> softmax per tile).  Costs 64 KiB of
 // shared memory (the K/V ring shrinks to 3 stages at D = 128).
 constexpr bool kPSmem = ATTN_P_SMEM != 0;
+#ifdef ATTN_TRACE
+constexpr bool kTraceBuild = true;    // the timeline trace instruments the non-persistent kernel
+#else
+constexpr bool kTraceBuild = false;
+#endif
 constexpr bool kToken = ATTN_TOKEN != 0;   // alternate the two softmax warpgroups' exp phases
 
 #ifdef ATTN_SOFTMAX_SPIN
@@ -753,9 +760,453 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ============================================================================
+// Persistent variant (D = 128, P in shared memory): one CTA per SM walks a
+// static snake schedule of work units (q-block, hq, b[, split]) -- head-major
+// with the heaviest causal q-blocks first, so the 148 concurrent units share a
+// few heads' K/V in L2 and the snake balances causal work like a dynamic
+// scheduler would.  Across units nothing drains: the K/V ring, the S/O TMEM
+// buffers and all barrier phases run on, the next unit's K tiles load while the
+// previous unit's last PV runs, and its first QK is issued as soon as its Q has
+// landed and S is free -- hiding the per-CTA prologue/epilogue a grid of
+// short-lived CTAs pays once per unit.  Shared memory holds two 64 KiB regions
+// that swap roles each unit: unit u keeps Q in region u&1 and P in region
+// (u+1)&1; the epilogue of unit u stages O in its Q region.  Q(u+1) therefore
+// loads into P(u)'s region once unit u's PVs are done (pv_done) and unit
+// u-1's O store has left it (epi_done).
+// ============================================================================
+// ATTN_PERSIST: 0 never, 1 for causal (no window) problems, 2 always.  Measured (r1g):
+// causal MHA 996 -> 1022 TFLOP/s (short, uneven units: the hidden boundaries matter);
+// non-causal MHA 1229 -> 1218 and the GQA window 1120 -> 1102 (long units, and the
+// persistent loop carries more live registers: 72 vs 52 bytes of spills).
+#ifndef ATTN_PERSIST
+#define ATTN_PERSIST 1
+#endif
+
+struct Unit {
+  int qblk, hq, zb, b, valid;
+};
+__device__ __forceinline__ Unit unit_of(const Shape& s, const VariantParams& v, int idx) {
+  const int nqb = (s.Sq + 2 * BM - 1) / (2 * BM);
+  const int nz = s.B * (s.kv_splits > 1 ? s.kv_splits : 1);
+  Unit u;
+  u.valid = idx < nqb * s.Hq * nz;
+  const int head_lin = idx / nqb, qi = idx % nqb;
+  u.qblk = v.causal ? nqb - 1 - qi : qi;          // heaviest causal q-block of a head first
+  u.hq = head_lin % s.Hq;
+  u.zb = head_lin / s.Hq;
+  u.b = s.kv_splits > 1 ? u.zb % s.B : u.zb;
+  return u;
+}
+// k-th unit of CTA c (snake order over rounds of gridDim.x units)
+__device__ __forceinline__ int unit_index(int k) {
+  const int G = gridDim.x, c = blockIdx.x;
+  return G * k + ((k & 1) ? G - 1 - c : c);
+}
+struct UnitRanges {
+  Range r0, r1;
+  int ulo, uhi, row0;
+  bool has_rows1;
+};
+__device__ __forceinline__ UnitRanges ranges_of(const Shape& s, const VariantParams& v, const Unit& u) {
+  UnitRanges q;
+  q.row0 = u.qblk * 2 * BM;
+  q.r0 = tile_range(s, v, q.row0);
+  q.r1 = tile_range(s, v, q.row0 + BM);
+  if (s.kv_splits > 1) {
+    const int t_lo = (u.zb / s.B) * s.kv_split_tiles, t_hi = t_lo + s.kv_split_tiles;
+    for (Range* r : {&q.r0, &q.r1}) {
+      r->lo = max(r->lo, t_lo);
+      r->hi = min(r->hi, t_hi);
+      if (r->lo >= r->hi) r->lo = r->hi = 0;
+    }
+  }
+  q.has_rows1 = q.row0 + BM < s.Sq;
+  q.ulo = q.uhi = 0;
+  const bool a0 = q.r0.hi > q.r0.lo, a1 = q.r1.hi > q.r1.lo;
+  if (a0 && a1) {
+    q.ulo = min(q.r0.lo, q.r1.lo);
+    q.uhi = max(q.r0.hi, q.r1.hi);
+  } else if (a0) {
+    q.ulo = q.r0.lo; q.uhi = q.r0.hi;
+  } else if (a1) {
+    q.ulo = q.r1.lo; q.uhi = q.r1.hi;
+  }
+  return q;
+}
+
+template <bool kAlibi, bool kSoftcap, bool kF16>
+__global__ void __launch_bounds__(kThreads, 1)
+    fwd_tc_persist_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                          const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
+                          const Shape s, const VariantParams v, float* __restrict__ lse) {
+  constexpr int D = 128;
+  constexpr int kRegion = 2 * BM * D * 2;                    // 64 KiB: two 128 x 128 16-bit tiles
+  constexpr int kTile = BM * D * 2;                          // 32 KiB
+  constexpr int kStages = 3;
+  constexpr int kKV = BN * D * 2;
+  constexpr bool kPlain = !kAlibi && !kSoftcap;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((smem_u32(smem) & 1023) != 0) __trap();
+  uint8_t* sKV = smem + 2 * kRegion;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + kStages * kKV);
+  uint64_t* q_full = bars;                 // [2] per region
+  uint64_t* kv_full = bars + 2;            // [3]
+  uint64_t* kv_empty = kv_full + kStages;  // [3]
+  uint64_t* s_full = kv_empty + kStages;   // [2] per tile
+  uint64_t* o_done = s_full + 2;           // [2] per tile
+  uint64_t* pv_done = o_done + 2;          // [1] all PVs of a unit done
+  uint64_t* epi_done = pv_done + 1;        // [2] per region: the O store staged in it has been read
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(epi_done + 2);
+  auto region = [&](int r) { return smem + r * kRegion; };
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  if (warp == kWarpLoad && lane == 0) {
+    prefetch_tmap(&tm_q);
+    prefetch_tmap(&tm_k);
+    prefetch_tmap(&tm_v);
+    prefetch_tmap(&tm_o);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&o_done[i], 1);
+      mbar_init(&epi_done[i], 2);
+    }
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    mbar_init(pv_done, 1);
+    fence_mbarrier_init();
+  }
+  if (warp == kWarpAlloc) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == kWarpLoad) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint64_t pol_q = policy_evict_first();
+      const uint64_t pol_kv = policy_evict_last();
+      int it = 0;
+      auto load_kv = [&](bool is_k, int jj, int hkv, int b) {
+        WAIT_LM(&kv_empty[it % kStages], ((it / kStages) & 1) ^ 1);
+        uint64_t* bar = &kv_full[it % kStages];
+        mbar_arrive_expect_tx(bar, kKV);
+        uint8_t* dst = sKV + (it % kStages) * kKV;
+        for (int bx = 0; bx < 2; ++bx)
+          tma_load_4d(is_k ? &tm_k : &tm_v, bar, dst + bx * BN * 128, bx * 64, jj * BN, hkv, b, pol_kv);
+        ++it;
+      };
+      for (int k = 0;; ++k) {
+        const Unit un = unit_of(s, v, unit_index(k));
+        if (!un.valid) break;
+        const UnitRanges ur = ranges_of(s, v, un);
+        const int hkv = un.hq / (s.Hq / s.Hkv);
+        if (ur.uhi > ur.ulo) {            // K tiles of this unit go first: they need no region
+          load_kv(true, ur.ulo, hkv, un.b);
+          if (ur.ulo + 1 < ur.uhi) load_kv(true, ur.ulo + 1, hkv, un.b);
+        }
+        // Q(k) -> region k&1, which held P(k-1) and the O staging of unit k-2
+        if (k >= 1) WAIT_LM(pv_done, (k - 1) & 1);
+        if (k >= 2) WAIT_LM(&epi_done[k & 1], ((k - 2) >> 1) & 1);
+        const int nq = ur.has_rows1 ? 2 : 1;
+        mbar_arrive_expect_tx(&q_full[k & 1], nq * kTile);
+        for (int t = 0; t < nq; ++t)
+          for (int bx = 0; bx < 2; ++bx)
+            tma_load_4d(&tm_q, &q_full[k & 1], region(k & 1) + t * kTile + bx * BM * 128, bx * 64, ur.row0 + t * BM,
+                        un.hq, un.b, pol_q);
+        for (int j = ur.ulo; j < ur.uhi; ++j) {
+          load_kv(false, j, hkv, un.b);
+          if (j + 2 < ur.uhi) load_kv(true, j + 2, hkv, un.b);
+        }
+      }
+    }
+  } else if (warp == kWarpMma) {
+    // ------------------------------------------------------------ MMA issuer (warp-wide)
+    constexpr uint32_t idesc_qk = idesc_f16_f32(BM, BN, 0, 0, !kF16);
+    constexpr uint32_t idesc_pv = idesc_f16_f32(BM, D, 0, 1, !kF16);
+    const uint32_t tS[2] = {tmem, tmem + 128};
+    const uint32_t tO[2] = {tmem + 256, tmem + 384};
+    int it = 0;
+    bool qk_any[2] = {false, false};
+    auto wait_tile = [&](int i) {
+      WAIT_LM(&kv_full[i % kStages], (i / kStages) & 1);
+      tc_fence_after();
+    };
+    for (int k = 0;; ++k) {
+      const Unit un = unit_of(s, v, unit_index(k));
+      if (!un.valid) break;
+      const UnitRanges ur = ranges_of(s, v, un);
+      const Range rg[2] = {ur.r0, ur.r1};
+      uint8_t* sQ = region(k & 1);
+      uint8_t* sP = region((k + 1) & 1);
+      auto qk = [&](int t, int i) {   // S_t = Q_t K^T (K tile in ring slot i)
+        if (qk_any[t]) {              // S_t free: its softmax threads hold the previous S_t
+          named_bar_sync(kBarS0 + t, kTileThreads + 32);
+          tc_fence_after();
+        }
+        qk_any[t] = true;
+        const uint32_t sq = smem_u32(sQ + t * kTile);
+        const uint32_t sk = smem_u32(sKV + (i % kStages) * kKV);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t ka = (kk >> 2) * (BM * 128) + (kk & 3) * 32;
+          const uint32_t kb = (kk >> 2) * (BN * 128) + (kk & 3) * 32;
+          mma_ss_warp(tS[t], smem_desc_sw128(sq + ka, 16, 1024), smem_desc_sw128(sk + kb, 16, 1024), idesc_qk,
+                      kk > 0 ? 1u : 0u);
+        }
+        mma_commit_warp(&s_full[t]);
+      };
+      auto pv = [&](int t, int i, bool acc) {   // O_t += P_t V (P from this unit's P region)
+        named_bar_sync(kBarP0 + t, kTileThreads + 32);
+        tc_fence_after();
+        const uint32_t sp = smem_u32(sP + t * kTile);
+        const uint32_t sv = smem_u32(sKV + (i % kStages) * kKV);
+#pragma unroll
+        for (int kk = 0; kk < BN / 16; ++kk) {
+          const uint32_t ka = (kk >> 2) * (BM * 128) + (kk & 3) * 32;
+          mma_ss_warp(tO[t], smem_desc_sw128(sp + ka, 16, 1024), smem_desc_sw128(sv + kk * 2048, BN * 128, 1024),
+                      idesc_pv, (acc || kk > 0) ? 1u : 0u);
+        }
+        mma_commit_warp(&o_done[t]);
+      };
+      // Q(k) must have landed even for a unit without KV work: pv_done #k may only
+      // complete after the producer has waited for #(k-1) (else its parity wait aliases).
+      WAIT_LM(&q_full[k & 1], (k >> 1) & 1);
+      tc_fence_after();
+      if (ur.uhi > ur.ulo) {
+        const int itK0 = it++;
+        const int itK1 = ur.ulo + 1 < ur.uhi ? it++ : -1;
+        wait_tile(itK0);
+        if (active(rg[0], ur.ulo)) qk(0, itK0);
+        if (active(rg[1], ur.ulo)) qk(1, itK0);
+        mma_commit_warp(&kv_empty[itK0 % kStages]);
+        if (itK1 >= 0) {
+          wait_tile(itK1);
+          if (active(rg[0], ur.ulo + 1)) qk(0, itK1);
+          if (active(rg[1], ur.ulo + 1)) qk(1, itK1);
+          mma_commit_warp(&kv_empty[itK1 % kStages]);
+        }
+        for (int j = ur.ulo; j < ur.uhi; ++j) {
+          const int itV = it++;
+          const bool k2 = j + 2 < ur.uhi;
+          const int itK = k2 ? it++ : 0;
+          wait_tile(itV);
+          if (active(rg[0], j)) pv(0, itV, j > rg[0].lo);
+          if (k2) {
+            wait_tile(itK);
+            if (active(rg[0], j + 2)) qk(0, itK);
+          }
+          if (active(rg[1], j)) pv(1, itV, j > rg[1].lo);
+          mma_commit_warp(&kv_empty[itV % kStages]);
+          if (k2) {
+            if (active(rg[1], j + 2)) qk(1, itK);
+            mma_commit_warp(&kv_empty[itK % kStages]);
+          }
+        }
+      }
+      mma_commit_warp(pv_done);       // every MMA of unit k (its P region is free once this lands)
+    }
+    for (int t = 0; t < 2; ++t)      // the softmax's arrival for its last S load
+      if (qk_any[t]) named_bar_sync(kBarS0 + t, kTileThreads + 32);
+  } else if (warp < kSoftmaxWarps) {
+    // ------------------------------------------------------------ softmax / correction / epilogue
+    const int t = (int)warp / 4;
+    const int wq = warp & 3;
+    const int r = wq * 32 + lane;
+    const int tid_t = (warp & 3) * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
+    const uint32_t tS = tmem + t * 128 + lane_off;
+    const uint32_t tO = tmem + 256 + t * 128 + lane_off;
+    uint32_t n_s = 0, n_pv = 0;            // S loads / PVs of this tile so far (barrier phases)
+    for (int k = 0;; ++k) {
+      const Unit un = unit_of(s, v, unit_index(k));
+      if (!un.valid) break;
+      const UnitRanges ur = ranges_of(s, v, un);
+      const Range R = t == 0 ? ur.r0 : ur.r1;
+      const int row0 = ur.row0;
+      const int hq = un.hq;
+      const int i = row0 + t * BM + r;
+      const long long qpos = v.q_off + i;
+      int jlo_row, jhi_row;
+      row_bounds(s, v, qpos, jlo_row, jhi_row);
+      const float nslope2 = kAlibi ? -v.alibi[hq] * kLog2e : 0.f;
+      uint8_t* sP = region((k + 1) & 1) + t * kTile;
+      float m_ref = -INFINITY, l = 0.f;
+      for (int j = R.lo; j < R.hi; ++j) {
+        mbar_wait(&s_full[t], n_s & 1);
+        ++n_s;
+        tc_fence_after();
+        float x[BN];
+        {
+          uint32_t u[BN];
+#pragma unroll
+          for (int c = 0; c < BN / 32; ++c) tmem_ld32(tS + c * 32, reinterpret_cast<uint32_t(&)[32]>(u[c * 32]));
+          tmem_ld_wait();
+          tc_fence_before();
+          named_bar_arrive(kBarS0 + t, kTileThreads + 32);   // S_t may be overwritten
+#pragma unroll
+          for (int c = 0; c < BN; ++c) x[c] = u2f(u[c]);
+        }
+        const bool need_mask = !(j * BN >= R.jlo_last && (j + 1) * BN - 1 <= R.jhi_first);
+        const int rel_lo = jlo_row - j * BN, rel_hi = jhi_row - j * BN;
+        const float dq0 = (float)(qpos - v.kv_off - (long long)j * BN);
+        const float mt = need_mask ? score_tile<kAlibi, kSoftcap, true>(x, v, nslope2, dq0, rel_lo, rel_hi)
+                                   : score_tile<kAlibi, kSoftcap, false>(x, v, nslope2, dq0, rel_lo, rel_hi);
+        const float m_run = fmaxf(m_ref, mt);
+        bool move, need_o;
+        if (m_ref == -INFINITY) {
+          move = m_run != -INFINITY;
+          need_o = false;
+        } else {
+          move = m_run - m_ref > kTau;
+          need_o = move;
+        }
+        float alpha = 1.f;
+        if (need_o) alpha = ex2_approx(m_ref - m_run);   // repair term h = exp(r - r') (Fig. 18d)
+        if (move) m_ref = m_run;
+        l *= alpha;
+        const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
+        if (n_pv > 0) {                 // PV_t of the previous step (maybe of the previous unit) is done
+          mbar_wait(&o_done[t], (n_pv - 1) & 1);
+          tc_fence_after();
+        }
+        float sum0 = 0.f, sum1 = 0.f;
+#pragma unroll
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            float a0, a1;
+            if constexpr (kPlain) {
+              a0 = fmaf(x[c0 + 2 * e], v.scale_log2, -m_use);
+              a1 = fmaf(x[c0 + 2 * e + 1], v.scale_log2, -m_use);
+            } else {
+              a0 = x[c0 + 2 * e] - m_use;
+              a1 = x[c0 + 2 * e + 1] - m_use;
+            }
+            const float p0 = ex2_approx(a0), p1 = ex2_approx(a1);
+            sum0 += p0;
+            sum1 += p1;
+            pk[e] = pack2<kF16>(p0, p1);
+          }
+          uint8_t* rowp = sP + (c0 >> 6) * (BM * 128) + r * 128;
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const int ch = ((c0 & 63) >> 3) + q4;
+            *reinterpret_cast<uint4*>(rowp + ((ch ^ (r & 7)) << 4)) =
+                make_uint4(pk[4 * q4], pk[4 * q4 + 1], pk[4 * q4 + 2], pk[4 * q4 + 3]);
+          }
+        }
+        if (__any_sync(0xffffffffu, need_o)) {   // O = h(O) (rare: lazy repair, R9)
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld32(tO + c * 32, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = f2u(u2f(o[e]) * alpha);
+            tmem_st32(tO + c * 32, o);
+          }
+          tmem_st_wait();
+        }
+        l += sum0 + sum1;
+        fence_proxy_async_smem();
+        tc_fence_before();
+        named_bar_arrive(kBarP0 + t, kTileThreads + 32);   // P_t(j) -> MMA issuer
+        ++n_pv;
+      }
+      // ---------------------------------------------------------- epilogue of unit k, tile t
+      const int n_it = R.hi - R.lo;
+      uint8_t* sOut = region(k & 1) + t * kTile;
+      const bool tile_rows = (row0 + t * BM) < s.Sq;
+      if (tile_rows) {
+        if (n_it > 0) {
+          mbar_wait(&o_done[t], (n_pv - 1) & 1);
+          tc_fence_after();
+        } else {
+          mbar_wait(&q_full[k & 1], (k >> 1) & 1);   // the Q tile we overwrite must have landed
+        }
+        const float inv_l = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t o[32];
+          if (n_it > 0) {
+            tmem_ld32(tO + c * 32, o);
+            tmem_ld_wait();
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = 0u;
+          }
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) pk[e] = pack2<kF16>(u2f(o[2 * e]) * inv_l, u2f(o[2 * e + 1]) * inv_l);
+          uint8_t* rowp = sOut + (c >> 1) * (BM * 128) + r * 128;
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const int ch = (c & 1) * 4 + q4;
+            *reinterpret_cast<uint4*>(rowp + ((ch ^ (r & 7)) << 4)) =
+                make_uint4(pk[4 * q4], pk[4 * q4 + 1], pk[4 * q4 + 2], pk[4 * q4 + 3]);
+          }
+        }
+        tc_fence_before();
+        fence_proxy_async_smem();
+        named_bar_sync(1 + t, kTileThreads);
+        if (tid_t == 0) {
+          for (int bx = 0; bx < 2; ++bx) tma_store_4d(&tm_o, sOut + bx * BM * 128, bx * 64, row0 + t * BM, hq, un.zb);
+          bulk_commit();
+          bulk_wait_read0();
+          mbar_arrive(&epi_done[k & 1]);
+        }
+        if (lse != nullptr && i < s.Sq)
+          lse[((size_t)un.zb * s.Hq + hq) * s.Sq + i] = l > 0.f ? m_ref * kLn2 + logf(l) : -INFINITY;
+        named_bar_sync(1 + t, kTileThreads);   // the staging tile is free again (P of unit k+1 goes there)
+      } else if (tid_t == 0) {
+        mbar_arrive(&epi_done[k & 1]);
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kWarpAlloc) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+int sm_count_of_current_device() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  int& c = cache[dev & 63];
+  if (c == 0 && cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) c = 148;
+  return c;
+}
+
+template <bool kAlibi, bool kSoftcap, bool kF16>
+cudaError_t launch_persist(const FwdTcArgs& a, cudaStream_t stream) {
+  constexpr int kSmem = 4 * (2 * BM * 128 * 2) / 2 + 3 * (BN * 128 * 2) + 16 * 8 + 16;   // 2 regions + ring + bars
+  cudaError_t e = set_smem_once<fwd_tc_persist_kernel<kAlibi, kSoftcap, kF16>>(kSmem);
+  if (e != cudaSuccess) return e;
+  const long long nqb = (a.s.Sq + 2 * BM - 1) / (2 * BM);
+  const long long units = nqb * a.s.Hq * a.s.B * (a.s.kv_splits > 1 ? a.s.kv_splits : 1);
+  const int grid = (int)std::min<long long>(units, sm_count_of_current_device());
+  fwd_tc_persist_kernel<kAlibi, kSoftcap, kF16>
+      <<<grid, kThreads, kSmem, stream>>>(a.tm_q, a.tm_k, a.tm_v, a.tm_o, a.s, a.v, a.lse);
+  return cudaGetLastError();
+}
+
 template <int D, bool kAlibi, bool kSoftcap, bool kF16>
 cudaError_t launch_t(const FwdTcArgs& a, cudaStream_t stream) {
   using C = Cfg<D>;
+  if constexpr (D == 128 && C::kPS && kHalves == 1 && !kTraceBuild) {
+    const bool pure_causal = a.v.causal && a.v.window_left < 0 && a.v.window_right < 0;
+    if (ATTN_PERSIST == 2 || (ATTN_PERSIST == 1 && pure_causal)) return launch_persist<kAlibi, kSoftcap, kF16>(a, stream);
+  }
   auto kern = fwd_tc_kernel<D, kAlibi, kSoftcap, kF16>;
   cudaError_t e = set_smem_once<fwd_tc_kernel<D, kAlibi, kSoftcap, kF16>>(C::kSmemBytes);
   if (e != cudaSuccess) return e;
