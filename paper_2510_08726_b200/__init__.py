@@ -80,16 +80,10 @@ def fused_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: Optio
     splits, n > 1 forces n splits."""
     lib = load()
     if q.device.type == "cpu":
-        dev = torch.device("cuda", torch.cuda.current_device())
-        qd, kd, vd = (t.to(dev, non_blocking=True) for t in (q, k, v))
-        sl = None if alibi_slopes is None else alibi_slopes.to(dev, non_blocking=True)
-        res = fused_fwd(qd, kd, vd, scale=scale, causal=causal, window=window, alibi_slopes=sl, softcap=softcap,
-                        q_pos_offset=q_pos_offset, kv_pos_offset=kv_pos_offset, seqlen_kv_total=seqlen_kv_total,
-                        return_lse=return_lse, stream=stream)
-        if return_lse:
-            o_d, l_d = res
-            return (o_d.to("cpu", non_blocking=False) if out is None else out.copy_(o_d)), l_d.cpu()
-        return res.to("cpu") if out is None else out.copy_(res)
+        return _fused_fwd_host(q, k, v, out=out, return_lse=return_lse, kv_splits=kv_splits,
+                               kw=dict(scale=scale, causal=causal, window=window, alibi_slopes=alibi_slopes,
+                                       softcap=softcap, q_pos_offset=q_pos_offset, kv_pos_offset=kv_pos_offset,
+                                       seqlen_kv_total=seqlen_kv_total))
     prob = _problem(q, k, scale=scale, causal=causal, window=window, alibi_slopes=alibi_slopes, softcap=softcap,
                     q_pos_offset=q_pos_offset, kv_pos_offset=kv_pos_offset, seqlen_kv_total=seqlen_kv_total)
     if out is None:
@@ -124,6 +118,46 @@ def _scratch(device, need: int, stream) -> torch.Tensor:
             stream.wait_stream(torch.cuda.current_stream(device))
         _SCRATCH[key] = ws
     return ws
+
+
+_HOST_STREAMS = {}
+
+
+def _fused_fwd_host(q, k, v, *, out, return_lse, kv_splits, kw, chunks: int = 8):
+    """End-to-end call on HOST tensors: the batch is cut into chunks that flow through two
+    CUDA streams, so the host->device copy of chunk c+1 overlaps the kernel and the
+    device->host copy of chunk c (pinned host memory makes the copies asynchronous).
+    Returns when the result is in host memory."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    streams = _HOST_STREAMS.get(dev.index)
+    if streams is None:
+        streams = _HOST_STREAMS[dev.index] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+    B = q.shape[0]
+    n = max(1, min(chunks, B))
+    bounds = [B * i // n for i in range(n + 1)]
+    pin = q.is_pinned()
+    if out is None:
+        out = torch.empty(q.shape, dtype=q.dtype, pin_memory=pin)
+    lse = torch.empty(q.shape[:3], dtype=torch.float32, pin_memory=pin) if return_lse else None
+    cur = torch.cuda.current_stream(dev)
+    sl = kw.pop("alibi_slopes")
+    for st in streams:
+        st.wait_stream(cur)
+    for c in range(n):
+        st = streams[c % 2]
+        b0, b1 = bounds[c], bounds[c + 1]
+        with torch.cuda.stream(st):
+            qd, kd, vd = (t[b0:b1].to(dev, non_blocking=True) for t in (q, k, v))
+            sld = None if sl is None else sl.to(dev, non_blocking=True)
+            res = fused_fwd(qd, kd, vd, alibi_slopes=sld, return_lse=return_lse, kv_splits=kv_splits,
+                            stream=st, **kw)
+            o_d, l_d = res if return_lse else (res, None)
+            out[b0:b1].copy_(o_d, non_blocking=True)
+            if lse is not None:
+                lse[b0:b1].copy_(l_d, non_blocking=True)
+    for st in streams:
+        st.synchronize()
+    return (out, lse) if return_lse else out
 
 
 class Parts:

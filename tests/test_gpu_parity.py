@@ -391,6 +391,25 @@ def test_host_buffers_end_to_end():
     assert_bf16_close(o.float().numpy().astype(np.float64), ref_o, "host e2e")
 
 
+def test_host_buffers_pipelined_chunks():
+    """The e2e path cuts the batch into chunks over two streams (copies overlap the kernel):
+    the result must equal the device call bit for bit, lse included, pinned or not."""
+    B, Hq, Hkv, S, D = 5, 4, 2, 300, 128
+    p = problem(B, Hq, Hkv, S, S, D, causal=True, alibi_slopes=datagen.alibi_slopes(Hq))
+    raw, f64 = gen_qkv(31338, B, Hq, Hkv, S, S, D)
+    ref_o, ref_l = oracle.attention(p, *f64)
+    dev = [dgd.to_device(x) for x in raw]
+    slopes = torch.tensor(np.asarray(p.alibi_slopes, dtype=np.float32))
+    o_dev, l_dev = pb.fused_fwd(*dev, causal=True, alibi_slopes=slopes.cuda(), return_lse=True)
+    for pinned in (True, False):
+        host = [t.cpu().pin_memory() if pinned else t.cpu() for t in dev]
+        o, l = pb.fused_fwd(*host, causal=True, alibi_slopes=slopes, return_lse=True)
+        assert o.device.type == "cpu" and l.device.type == "cpu"
+        assert torch.equal(o, o_dev.cpu()) and torch.equal(l, l_dev.cpu())
+    assert_bf16_close(o.float().numpy().astype(np.float64), ref_o, "host e2e chunks")
+    assert_lse_close(l.numpy(), ref_l, LSE_TOL_BF16, "host e2e lse")
+
+
 # --------------------------------------------------------------------------- fp16 inputs (NEXT-1, the paper's precision P:946)
 def test_device_generator_fp16_is_bit_identical():
     host = datagen.tensor(999, 3, (2, 3, 50, 64), "f16")
