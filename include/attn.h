@@ -165,8 +165,13 @@ ATTN_API attn_status attn_fused_fwd_splitkv(const attn_problem* prob, attn_tenso
                                             size_t workspace_bytes, attn_stream_t stream);
 
 /* ---------------------------------------------------------------------
- * Split-K Update decode (Alg. 2, Fig. 5): seqlen_q must be 1, dtype bf16 or fp16,
- * D in {64, 128}.  The KV axis of every (b, hkv) is cut into num_splits
+ * Split-K Update decode (Alg. 2, Fig. 5): dtype bf16 or fp16, D in {64, 128},
+ * seqlen_q = 1 -- or a few query tokens (multi-token / speculative decode,
+ * NEXT-2) with G * seqlen_q <= 16, G = heads_q / heads_kv: the G * seqlen_q
+ * (head, query) rows of a KV group share one 16-row tensor-core tile, each
+ * with its own causal / window mask (bottom-right positions as everywhere).
+ * seqlen_q > 1 needs parts_out == NULL (the fused combine), o != NULL, and
+ * writes lse as [B][Hq][Sq].  The KV axis of every (b, hkv) is cut into num_splits
  * contiguous parts (PrivatizeReduce); each CTA streams its part
  * of K and V once from HBM for all G query heads of the group and emits one
  * partial triple per (part, b, hq).  Then the global section (Eq. 8)

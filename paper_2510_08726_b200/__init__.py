@@ -228,7 +228,8 @@ def splitkv_decode(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, num_spl
                    seqlen_kv_total: Optional[int] = None, out: Optional[torch.Tensor] = None,
                    lse: Optional[torch.Tensor] = None, return_lse: bool = False, parts: Optional[Parts] = None,
                    workspace: Optional[torch.Tensor] = None, want_out: bool = True, stream=None):
-    """Split-K Update decode (``attn_splitkv_decode``): q [B, Hq, 1, D] bf16.
+    """Split-K Update decode (``attn_splitkv_decode``): q [B, Hq, Sq, D] bf16/fp16 with
+    Sq = 1, or a few query tokens (multi-token decode) with G * Sq <= 16 packed rows.
 
     ``parts`` receives the raw local-section triples; with ``want_out`` the
     Eq. 8 combine also produces O (and lse) -- fused into the split kernel
@@ -254,8 +255,8 @@ def splitkv_decode(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, num_spl
         out = torch.empty_like(q, memory_format=torch.contiguous_format)
     if not want_out:
         out = None
-    if return_lse and lse is None and want_out:
-        lse = torch.empty(q.shape[:2], device=q.device, dtype=torch.float32)
+    if return_lse and lse is None and want_out:   # [B, Hq] for one query, else [B, Hq, Sq]
+        lse = torch.empty(q.shape[:2] if q.shape[2] == 1 else q.shape[:3], device=q.device, dtype=torch.float32)
     ws_ptr, ws_bytes = None, 0
     if parts is None:
         need = lib.attn_splitkv_workspace_bytes(ctypes.byref(prob), num_splits)

@@ -299,7 +299,7 @@ int32_t attn_splitkv_default_splits(const attn_problem* p, int32_t sm_count) {
 size_t attn_splitkv_workspace_bytes(const attn_problem* p, int32_t num_splits) {
   if (p == nullptr) return 0;
   if (num_splits <= 0) num_splits = attn_splitkv_default_splits(p, 0);
-  const size_t rows = (size_t)num_splits * p->batch * p->heads_q;
+  const size_t rows = (size_t)num_splits * p->batch * p->heads_q * (p->seqlen_q > 1 ? p->seqlen_q : 1);
   auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
   // the fused combine's arrival tickets [B][Hkv] (zero between calls), then m | l | O partials
   return up((size_t)p->batch * p->heads_kv * 4) + up(rows * 4) * 2 + up(rows * p->head_dim * 4);
@@ -313,19 +313,27 @@ attn_status attn_splitkv_decode(const attn_problem* prob, attn_tensor q, attn_te
   attn_status st = check_problem(prob, &vp);
   if (st != ATTN_OK) return st;
   const attn_problem& p = *prob;
-  if (p.seqlen_q != 1) return fail(ATTN_ERR_UNSUPPORTED, "decode requires seqlen_q == 1 (got %d)", p.seqlen_q);
   if (p.dtype == ATTN_FP32) return fail(ATTN_ERR_UNSUPPORTED, "decode supports bf16 and fp16 only");
   if (p.head_dim != 64 && p.head_dim != 128)
     return fail(ATTN_ERR_UNSUPPORTED, "decode head_dim must be 64 or 128 (got %d)", p.head_dim);
   const int G = p.heads_q / p.heads_kv;
-  if (G > 8) return fail(ATTN_ERR_UNSUPPORTED, "decode supports GQA groups up to 8 (got %d)", G);
+  const int Sq = p.seqlen_q;
+  // the G * Sq (head, query) rows of a KV group are packed into one 16-row mma tile
+  if ((int64_t)G * Sq > 16)
+    return fail(ATTN_ERR_UNSUPPORTED, "decode packs G * seqlen_q <= 16 rows (got %d x %d); use attn_fused_fwd",
+                G, Sq);
   CHECK_ARG(parts_out != nullptr || o.ptr != nullptr, "decode needs parts_out or o");
+  if (Sq > 1 && parts_out != nullptr)
+    return fail(ATTN_ERR_UNSUPPORTED, "parts_out (a per-(b, h) triple) needs seqlen_q == 1");
   if (num_splits < 0) return fail(ATTN_ERR_INVALID_ARGUMENT, "num_splits must be >= 0");
   if (num_splits == 0) num_splits = attn_splitkv_default_splits(prob, 0);
-  if ((st = check_tensor(q, "q", 2, p.batch, p.heads_q, 1)) != ATTN_OK) return st;
+  if (Sq > 1 && num_splits > attn::decode_fused_max_splits(G * Sq, p.head_dim))
+    return fail(ATTN_ERR_UNSUPPORTED, "seqlen_q > 1 supports at most %d splits",
+                attn::decode_fused_max_splits(G * Sq, p.head_dim));
+  if ((st = check_tensor(q, "q", 2, p.batch, p.heads_q, Sq)) != ATTN_OK) return st;
   if ((st = check_tensor(k, "k", 2, p.batch, p.heads_kv, p.seqlen_kv)) != ATTN_OK) return st;
   if ((st = check_tensor(v, "v", 2, p.batch, p.heads_kv, p.seqlen_kv)) != ATTN_OK) return st;
-  if (o.ptr != nullptr && (st = check_tensor(o, "o", 2, p.batch, p.heads_q, 1)) != ATTN_OK) return st;
+  if (o.ptr != nullptr && (st = check_tensor(o, "o", 2, p.batch, p.heads_q, Sq)) != ATTN_OK) return st;
 
   attn::DecodeArgs a{};
   a.s = shape_of(prob);
@@ -334,6 +342,7 @@ attn_status attn_splitkv_decode(const attn_problem* prob, attn_tensor q, attn_te
   a.q = static_cast<const uint16_t*>(q.ptr);
   a.q_sb = q.stride_b;
   a.q_sh = q.stride_h;
+  a.q_ss = q.stride_s;
   const int nk = attn::decode_stage_keys(G, p.head_dim);
   a.num_splits = num_splits;
   const int64_t per = (p.seqlen_kv + num_splits - 1) / num_splits;
@@ -349,24 +358,26 @@ attn_status attn_splitkv_decode(const attn_problem* prob, attn_tensor q, attn_te
     const size_t need = attn_splitkv_workspace_bytes(prob, num_splits);
     if (workspace == nullptr || workspace_bytes < need)
       return fail(ATTN_ERR_WORKSPACE_TOO_SMALL, "workspace needs %zu bytes", need);
-    const size_t rows = (size_t)num_splits * p.batch * p.heads_q;
+    const size_t rows = (size_t)num_splits * p.batch * p.heads_q * Sq;
     auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
     char* const w0 = static_cast<char*>(workspace);
     char* w = w0 + up((size_t)p.batch * p.heads_kv * 4);   // after the ticket block
     float* m = reinterpret_cast<float*>(w);
     float* l = reinterpret_cast<float*>(w + up(rows * 4));
     float* ob = reinterpret_cast<float*>(w + 2 * up(rows * 4));
-    const long long bh = (long long)p.batch * p.heads_q;
-    a.parts = attn::PartsView{m, l, ob, num_splits, bh, p.heads_q, 1, bh * p.head_dim,
-                              (long long)p.heads_q * p.head_dim, p.head_dim};
+    // [split][b][hq][i] (m, l) and [split][b][hq][i][d] (O); the kernel adds i (and i * D)
+    const long long bhs = (long long)p.batch * p.heads_q * Sq;
+    a.parts = attn::PartsView{m, l, ob, num_splits, bhs, (long long)p.heads_q * Sq, Sq, bhs * p.head_dim,
+                              (long long)p.heads_q * Sq * p.head_dim, (long long)Sq * p.head_dim};
     // Fused Eq. 8 combine (last CTA per (b, hkv)) when the output is wanted and the
     // split weights fit the kernel's staging area; else the separate combine kernel.
-    if (o.ptr != nullptr && num_splits <= attn::decode_fused_max_splits(G, p.head_dim)) {
+    if (o.ptr != nullptr && num_splits <= attn::decode_fused_max_splits(G * Sq, p.head_dim)) {
       a.tickets = reinterpret_cast<unsigned*>(w0);
       a.out_f16 = p.dtype == ATTN_FP16 ? 1 : 0;
       a.o = o.ptr;
       a.o_sb = o.stride_b;
       a.o_sh = o.stride_h;
+      a.o_ss = o.stride_s;
       a.lse = lse;
     }
   }

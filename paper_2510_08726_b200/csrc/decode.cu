@@ -80,7 +80,9 @@ __device__ __forceinline__ uint32_t tile_off(int key, int ch) {
   return (ch >> 3) * (NK * 128) + key * 128 + (((ch & 7) ^ (key & 7)) << 4);
 }
 
-template <int D, bool kAlibi, bool kSoftcap, bool kF16>
+// kHi: the packed (head, query) rows reach past 8 (G * Sq in 9..16): rows g + 8 of the
+// m16n8k16 tiles carry data too (multi-token decode, NEXT-2).
+template <int D, bool kAlibi, bool kSoftcap, bool kF16, bool kHi>
 __global__ void __launch_bounds__(kThreads) decode_split_kernel(const __grid_constant__ CUtensorMap tm_k,
                                                                 const __grid_constant__ CUtensorMap tm_v,
                                                                 const DecodeArgs a) {
@@ -127,37 +129,83 @@ __global__ void __launch_bounds__(kThreads) decode_split_kernel(const __grid_con
   }
 
   // ------------------------------------------------------------ consumers
+  // Packed mma rows: rho = h * Sq + i (query head h of the group, query i); thread-quad
+  // group g owns rows g (fragment halves 0/1) and g + 8 (halves 2/3, only with kHi).
   const VariantParams& v = a.v;
-  const int row = lane >> 2;          // mma row = query head within the group (rows >= G are padding)
+  const int Sq = a.s.Sq;
+  const int nrows = G * Sq;
   const int quad = lane & 3;
-  const bool row_ok = row < G;
-  const int hq = hkv * G + (row_ok ? row : 0);
-  const long long qpos = v.q_off;     // Sq = 1
-  // Q as the A operand: rows = heads (zero beyond G); loaded once.
+  const int r_lo = lane >> 2, r_hi = r_lo + 8;
+  const bool ok_lo = r_lo < nrows, ok_hi = kHi && r_hi < nrows;
+  const int h_lo = ok_lo ? r_lo / Sq : 0, i_lo = ok_lo ? r_lo % Sq : 0;
+  const int h_hi = ok_hi ? r_hi / Sq : 0, i_hi = ok_hi ? r_hi % Sq : 0;
+  const int hq_lo = hkv * G + h_lo, hq_hi = hkv * G + h_hi;
+  const long long qpos_lo = v.q_off + i_lo, qpos_hi = v.q_off + i_hi;
+  // Q as the A operand: rows = packed (head, query) pairs (zero beyond nrows); loaded once.
   uint32_t qa[D / 16][4];
   {
-    const uint16_t* qrow = a.q + (long long)b * a.q_sb + (long long)hq * a.q_sh;
+    const uint16_t* q_lo = a.q + (long long)b * a.q_sb + (long long)hq_lo * a.q_sh + (long long)i_lo * a.q_ss;
+    const uint16_t* q_hi = a.q + (long long)b * a.q_sb + (long long)hq_hi * a.q_sh + (long long)i_hi * a.q_ss;
 #pragma unroll
     for (int kk = 0; kk < D / 16; ++kk) {
       const int d0 = kk * 16 + quad * 2;
-      qa[kk][0] = row_ok ? *reinterpret_cast<const uint32_t*>(qrow + d0) : 0u;
-      qa[kk][1] = 0u;  // rows 8..15
-      qa[kk][2] = row_ok ? *reinterpret_cast<const uint32_t*>(qrow + d0 + 8) : 0u;
-      qa[kk][3] = 0u;
+      qa[kk][0] = ok_lo ? *reinterpret_cast<const uint32_t*>(q_lo + d0) : 0u;
+      qa[kk][1] = ok_hi ? *reinterpret_cast<const uint32_t*>(q_hi + d0) : 0u;
+      qa[kk][2] = ok_lo ? *reinterpret_cast<const uint32_t*>(q_lo + d0 + 8) : 0u;
+      qa[kk][3] = ok_hi ? *reinterpret_cast<const uint32_t*>(q_hi + d0 + 8) : 0u;
     }
   }
-  // allowed key interval of this query (local indices), intersected with the split
-  long long jlo = ks, jhi = ke - 1;
-  if (v.window_left >= 0) jlo = max(jlo, qpos - v.window_left - v.kv_off);
-  if (v.causal) jhi = min(jhi, qpos - v.kv_off);
-  if (v.window_right >= 0) jhi = min(jhi, qpos + v.window_right - v.kv_off);
-  const float nslope2 = (kAlibi && row_ok) ? -v.alibi[hq] * kLog2e : 0.f;
+  // allowed key interval of each row's query (local indices), intersected with the split
+  auto bounds = [&](long long qpos, long long& jlo, long long& jhi) {
+    jlo = ks;
+    jhi = ke - 1;
+    if (v.window_left >= 0) jlo = max(jlo, qpos - v.window_left - v.kv_off);
+    if (v.causal) jhi = min(jhi, qpos - v.kv_off);
+    if (v.window_right >= 0) jhi = min(jhi, qpos + v.window_right - v.kv_off);
+  };
+  long long jlo_lo, jhi_lo, jlo_hi = 0, jhi_hi = -1;
+  bounds(qpos_lo, jlo_lo, jhi_lo);
+  if (kHi) bounds(qpos_hi, jlo_hi, jhi_hi);
+  const float ns_lo = (kAlibi && ok_lo) ? -v.alibi[hq_lo] * kLog2e : 0.f;
+  const float ns_hi = (kAlibi && ok_hi) ? -v.alibi[hq_hi] * kLog2e : 0.f;
 
-  float m = -INFINITY;   // running max of this warp's keys for row `row` (log2 units)
-  float l = 0.f;         // per-thread partial of the running denominator
+  float m_lo = -INFINITY, m_hi = -INFINITY;   // running max of this warp's keys per row (log2 units)
+  float l_lo = 0.f, l_hi = 0.f;               // per-thread partials of the running denominators
   float o[D / 8][4];
 #pragma unroll
   for (int n = 0; n < D / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+
+  // one row half: score_mod + mask (log2 units), quad-max, repair, p = exp(x - m)
+  auto row_step = [&](const float (&sv)[2][4], int hoff, long long qpos, long long jlo, long long jhi, float nsl,
+                      bool ok, int key0, float& m, float& l, float (&p)[4]) -> float {
+    float x[4];
+#pragma unroll
+    for (int n = 0; n < 2; ++n)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = key0 + n * 8 + quad * 2 + e;
+        float xv = sv[n][hoff + e];
+        if constexpr (kSoftcap) {
+          xv = v.softcap_log2 * tanh_approx(xv * v.scale_over_cap);
+        } else {
+          xv *= v.scale_log2;
+        }
+        if constexpr (kAlibi) xv = fmaf(nsl, fabsf((float)(qpos - v.kv_off - j)), xv);
+        x[n * 2 + e] = (j >= jlo && j <= jhi && ok) ? xv : -INFINITY;
+      }
+    float mt = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
+    mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 1));
+    mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 2));
+    const float m_new = fmaxf(m, mt);
+    // repair term exp(m_old - m_new) (Fig. 18d); guards for rows still empty
+    const float alpha = (m == -INFINITY) ? 0.f : ex2_approx(m - m_new);
+    const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) p[e] = ex2_approx(x[e] - m_use);
+    l = l * alpha + (p[0] + p[1] + p[2] + p[3]);
+    m = m_new;
+    return alpha;
+  };
 
   for (int st = 0; st < nstage; ++st) {
     const int slot = st % kStages;
@@ -167,7 +215,7 @@ __global__ void __launch_bounds__(kThreads) decode_split_kernel(const __grid_con
     const int kb = warp * kKeysPerWarp;   // this warp's 16 keys of the stage
 
     // S (16 rows x 16 keys) = Q K^T
-    float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    float s4[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
     {
       const int key = kb + (lane & 7) + ((lane >> 4) << 3);
       const int sub = (lane >> 3) & 1;
@@ -175,50 +223,30 @@ __global__ void __launch_bounds__(kThreads) decode_split_kernel(const __grid_con
       for (int kk = 0; kk < D / 16; ++kk) {
         uint32_t b0, b1, b2, b3;
         ldsm_x4(sk + tile_off(key, kk * 2 + sub), b0, b1, b2, b3);
-        mma16816<kF16>(s[0], qa[kk], b0, b1);
-        mma16816<kF16>(s[1], qa[kk], b2, b3);
+        mma16816<kF16>(s4[0], qa[kk], b0, b1);
+        mma16816<kF16>(s4[1], qa[kk], b2, b3);
       }
     }
-    // score_mod + mask (log2 units); this thread holds keys kb + n*8 + quad*2 + e of row `row`
     const int key0 = ks + st * NK + kb;
-    float x[4];
-#pragma unroll
-    for (int n = 0; n < 2; ++n)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int j = key0 + n * 8 + quad * 2 + e;
-        float xv = s[n][e];
-        if constexpr (kSoftcap) {
-          xv = v.softcap_log2 * tanh_approx(xv * v.scale_over_cap);
-        } else {
-          xv *= v.scale_log2;
-        }
-        if constexpr (kAlibi) xv = fmaf(nslope2, fabsf((float)(qpos - v.kv_off - j)), xv);
-        x[n * 2 + e] = (j >= jlo && j <= jhi && row_ok) ? xv : -INFINITY;
-      }
-    float mt = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
-    mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 1));
-    mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 2));
-    const float m_new = fmaxf(m, mt);
-    // repair term exp(m_old - m_new) (Fig. 18d); guards for rows still empty
-    const float alpha = (m == -INFINITY) ? 0.f : ex2_approx(m - m_new);
-    const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
-    float p[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) p[e] = ex2_approx(x[e] - m_use);
-    l = l * alpha + (p[0] + p[1] + p[2] + p[3]);
-    m = m_new;
+    float p_lo[4], p_hi[4] = {0.f, 0.f, 0.f, 0.f};
+    const float a_lo = row_step(s4, 0, qpos_lo, jlo_lo, jhi_lo, ns_lo, ok_lo, key0, m_lo, l_lo, p_lo);
+    float a_hi = 1.f;
+    if constexpr (kHi) a_hi = row_step(s4, 2, qpos_hi, jlo_hi, jhi_hi, ns_hi, ok_hi, key0, m_hi, l_hi, p_hi);
 #pragma unroll
     for (int n = 0; n < D / 8; ++n) {
-      o[n][0] *= alpha;
-      o[n][1] *= alpha;
+      o[n][0] *= a_lo;
+      o[n][1] *= a_lo;
+      if constexpr (kHi) {
+        o[n][2] *= a_hi;
+        o[n][3] *= a_hi;
+      }
     }
-    // P as the A operand (rows 8..15 zero)
+    // P as the A operand: rows g (keys 2t.., 2t+8..) and g + 8
     uint32_t pa[4];
-    pa[0] = pack2<kF16>(p[0], p[1]);
-    pa[1] = 0u;
-    pa[2] = pack2<kF16>(p[2], p[3]);
-    pa[3] = 0u;
+    pa[0] = pack2<kF16>(p_lo[0], p_lo[1]);
+    pa[1] = kHi ? pack2<kF16>(p_hi[0], p_hi[1]) : 0u;
+    pa[2] = pack2<kF16>(p_lo[2], p_lo[3]);
+    pa[3] = kHi ? pack2<kF16>(p_hi[2], p_hi[3]) : 0u;
     // O (16 x D) += P V
     {
       const int key = kb + (lane & 7) + (((lane >> 3) & 1) << 3);
@@ -236,43 +264,62 @@ __global__ void __launch_bounds__(kThreads) decode_split_kernel(const __grid_con
   }
 
   // ------------------------------------------------------------ merge the 4 warps (Eq. 8) and emit
-  l += __shfl_xor_sync(0xffffffffu, l, 1);
-  l += __shfl_xor_sync(0xffffffffu, l, 2);
+  l_lo += __shfl_xor_sync(0xffffffffu, l_lo, 1);
+  l_lo += __shfl_xor_sync(0xffffffffu, l_lo, 2);
+  if constexpr (kHi) {
+    l_hi += __shfl_xor_sync(0xffffffffu, l_hi, 1);
+    l_hi += __shfl_xor_sync(0xffffffffu, l_hi, 2);
+  }
   // every stage's smem is free now: reuse it for the reduction
   named_bar_sync(1, kConsumerWarps * 32);
   float* red = reinterpret_cast<float*>(smem);   // [warp][16 rows][D + 2]
-  float* rw = red + (warp * 16 + row) * (D + 2);
+  {
+    float* rw = red + (warp * 16 + r_lo) * (D + 2);
 #pragma unroll
-  for (int n = 0; n < D / 8; ++n) {
-    rw[n * 8 + quad * 2] = o[n][0];
-    rw[n * 8 + quad * 2 + 1] = o[n][1];
-  }
-  if (quad == 0) {
-    rw[D] = m;
-    rw[D + 1] = l;
+    for (int n = 0; n < D / 8; ++n) {
+      rw[n * 8 + quad * 2] = o[n][0];
+      rw[n * 8 + quad * 2 + 1] = o[n][1];
+    }
+    if (quad == 0) {
+      rw[D] = m_lo;
+      rw[D + 1] = l_lo;
+    }
+    if constexpr (kHi) {
+      float* rh = red + (warp * 16 + r_hi) * (D + 2);
+#pragma unroll
+      for (int n = 0; n < D / 8; ++n) {
+        rh[n * 8 + quad * 2] = o[n][2];
+        rh[n * 8 + quad * 2 + 1] = o[n][3];
+      }
+      if (quad == 0) {
+        rh[D] = m_hi;
+        rh[D + 1] = l_hi;
+      }
+    }
   }
   named_bar_sync(1, kConsumerWarps * 32);
-  for (int e = threadIdx.x; e < G * D; e += kConsumerWarps * 32) {
-    const int h = e / D, d = e % D;
+  for (int e = threadIdx.x; e < nrows * D; e += kConsumerWarps * 32) {
+    const int rho = e / D, d = e % D;
     float M = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, red[(w * 16 + h) * (D + 2) + D]);
+    for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, red[(w * 16 + rho) * (D + 2) + D]);
     float L = 0.f, O = 0.f;
     if (M != -INFINITY) {
 #pragma unroll
       for (int w = 0; w < kConsumerWarps; ++w) {
-        const float* r = red + (w * 16 + h) * (D + 2);
+        const float* r = red + (w * 16 + rho) * (D + 2);
         const float mw = r[D];
         const float wgt = (mw == -INFINITY) ? 0.f : ex2_approx(mw - M);
         L = fmaf(wgt, r[D + 1], L);
         O = fmaf(wgt, r[d], O);
       }
     }
-    const int hh = hkv * G + h;
-    float* po = a.parts.o + split * a.parts.o_sp + (long long)b * a.parts.o_sb + (long long)hh * a.parts.o_sh;
+    const int hh = hkv * G + rho / Sq, qi = rho % Sq;
+    float* po = a.parts.o + split * a.parts.o_sp + (long long)b * a.parts.o_sb + (long long)hh * a.parts.o_sh +
+                (long long)qi * D;
     po[d] = O;
     if (d == 0) {
-      const long long mi = split * a.parts.m_sp + (long long)b * a.parts.m_sb + (long long)hh * a.parts.m_sh;
+      const long long mi = split * a.parts.m_sp + (long long)b * a.parts.m_sb + (long long)hh * a.parts.m_sh + qi;
       a.parts.m[mi] = M * kLn2;   // natural-log units (ABI)
       a.parts.l[mi] = L;
     }
@@ -291,11 +338,11 @@ __global__ void __launch_bounds__(kThreads) decode_split_kernel(const __grid_con
   if (!s_last) return;
   __threadfence();
   const int S = a.num_splits;
-  float* wts = red;                       // [G][S] weights exp(m_s - M) / L (smem reused)
-  float* stat = red + G * S;              // [G][2]: M (natural log), L
-  for (int h = warp; h < G; h += kConsumerWarps) {   // warp reduces head h over the splits
-    const int hh = hkv * G + h;
-    const long long mb = (long long)b * a.parts.m_sb + (long long)hh * a.parts.m_sh;
+  float* wts = red;                       // [nrows][S] weights exp(m_s - M) (smem reused)
+  float* stat = red + nrows * S;          // [nrows][2]: M (natural log), L
+  for (int rho = warp; rho < nrows; rho += kConsumerWarps) {   // warp reduces row rho over the splits
+    const int hh = hkv * G + rho / Sq, qi = rho % Sq;
+    const long long mb = (long long)b * a.parts.m_sb + (long long)hh * a.parts.m_sh + qi;
     float M = -INFINITY;
     for (int sp = lane; sp < S; sp += 32) M = fmaxf(M, __ldcg(a.parts.m + sp * a.parts.m_sp + mb));
 #pragma unroll
@@ -304,30 +351,30 @@ __global__ void __launch_bounds__(kThreads) decode_split_kernel(const __grid_con
     for (int sp = lane; sp < S; sp += 32) {
       const float ms = __ldcg(a.parts.m + sp * a.parts.m_sp + mb);
       const float w = (ms == -INFINITY) ? 0.f : expf(ms - M);   // repair term exp(max_s - max_g)
-      wts[h * S + sp] = w;
+      wts[rho * S + sp] = w;
       L = fmaf(w, __ldcg(a.parts.l + sp * a.parts.m_sp + mb), L);
     }
 #pragma unroll
     for (int o2 = 16; o2 > 0; o2 >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o2);
     if (lane == 0) {
-      stat[h * 2] = M;
-      stat[h * 2 + 1] = L;
+      stat[rho * 2] = M;
+      stat[rho * 2 + 1] = L;
     }
   }
   named_bar_sync(1, kConsumerWarps * 32);
-  for (int e = threadIdx.x; e < G * D; e += kConsumerWarps * 32) {
-    const int h = e / D, d = e % D;
-    const int hh = hkv * G + h;
-    const float L = stat[h * 2 + 1];
-    const float* po = a.parts.o + (long long)b * a.parts.o_sb + (long long)hh * a.parts.o_sh + d;
+  for (int e = threadIdx.x; e < nrows * D; e += kConsumerWarps * 32) {
+    const int rho = e / D, d = e % D;
+    const int hh = hkv * G + rho / Sq, qi = rho % Sq;
+    const float L = stat[rho * 2 + 1];
+    const float* po = a.parts.o + (long long)b * a.parts.o_sb + (long long)hh * a.parts.o_sh + (long long)qi * D + d;
     float acc = 0.f;
     if (L > 0.f)
-      for (int sp = 0; sp < S; ++sp) acc = fmaf(wts[h * S + sp], __ldcg(po + sp * a.parts.o_sp), acc);
+      for (int sp = 0; sp < S; ++sp) acc = fmaf(wts[rho * S + sp], __ldcg(po + sp * a.parts.o_sp), acc);
     const float out = L > 0.f ? acc / L : 0.f;
-    const long long oi = (long long)b * a.o_sb + (long long)hh * a.o_sh + d;
+    const long long oi = (long long)b * a.o_sb + (long long)hh * a.o_sh + (long long)qi * a.o_ss + d;
     if (a.out_f16) reinterpret_cast<__half*>(a.o)[oi] = __float2half_rn(out);
     else reinterpret_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(out);
-    if (d == 0 && a.lse) a.lse[(long long)b * a.s.Hq + hh] = L > 0.f ? stat[h * 2] + logf(L) : -INFINITY;
+    if (d == 0 && a.lse) a.lse[((long long)b * a.s.Hq + hh) * Sq + qi] = L > 0.f ? stat[rho * 2] + logf(L) : -INFINITY;
   }
   if (threadIdx.x == 0) *ticket = 0u;     // ready for the next call
 }
@@ -451,15 +498,21 @@ __global__ void __launch_bounds__(128) merge_kernel(const MergeArgs a) {
   if (a.lse_out && lane == 0) a.lse_out[row] = L > 0.f ? M + logf(L) : -INFINITY;
 }
 
-template <int D, bool kAlibi, bool kSoftcap, bool kF16>
-cudaError_t launch_dec_t(const DecodeArgs& a, cudaStream_t stream) {
+template <int D, bool kAlibi, bool kSoftcap, bool kF16, bool kHi>
+cudaError_t launch_dec_h(const DecodeArgs& a, cudaStream_t stream) {
   using C = DCfg<D>;
-  auto kern = decode_split_kernel<D, kAlibi, kSoftcap, kF16>;
-  cudaError_t e = set_smem_once<decode_split_kernel<D, kAlibi, kSoftcap, kF16>>(C::kSmemBytes);
+  auto kern = decode_split_kernel<D, kAlibi, kSoftcap, kF16, kHi>;
+  cudaError_t e = set_smem_once<decode_split_kernel<D, kAlibi, kSoftcap, kF16, kHi>>(C::kSmemBytes);
   if (e != cudaSuccess) return e;
   dim3 grid(a.num_splits, a.s.Hkv, a.s.B);
   kern<<<grid, kThreads, C::kSmemBytes, stream>>>(a.tm_k, a.tm_v, a);
   return cudaGetLastError();
+}
+
+template <int D, bool kAlibi, bool kSoftcap, bool kF16>
+cudaError_t launch_dec_t(const DecodeArgs& a, cudaStream_t stream) {
+  return (a.s.Hq / a.s.Hkv) * a.s.Sq > 8 ? launch_dec_h<D, kAlibi, kSoftcap, kF16, true>(a, stream)
+                                         : launch_dec_h<D, kAlibi, kSoftcap, kF16, false>(a, stream);
 }
 
 template <int D, bool kF16>
@@ -474,10 +527,10 @@ cudaError_t launch_dec_d(const DecodeArgs& a, cudaStream_t stream) {
 }  // namespace
 
 int decode_stage_keys(int, int) { return NK; }
-int decode_fused_max_splits(int G, int D) {
-  // the fused combine stages [G][S] weights + [G][2] stats in the (then idle) stage ring
+int decode_fused_max_splits(int rows, int D) {
+  // the fused combine stages [rows][S] weights + [rows][2] stats in the (then idle) stage ring
   const int bytes = kStages * 2 * NK * D * 2;
-  return bytes / (4 * G) - 2;
+  return bytes / (4 * rows) - 2;
 }
 
 cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t stream, int* launches) {

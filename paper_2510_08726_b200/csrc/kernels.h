@@ -76,7 +76,7 @@ struct DecodeArgs {
   bool f16;                     // fp16 inputs (else bf16)
   VariantParams v;
   const uint16_t* q;            // bf16 / fp16 bits
-  long long q_sb, q_sh;
+  long long q_sb, q_sh, q_ss;
   int num_splits, split_len;    // keys per split (multiple of the stage size)
   PartsView parts;              // destination of the local-section triples
   CUtensorMap tm_k, tm_v;       // [D x Skv x Hkv x B], box (D, NK)
@@ -84,12 +84,12 @@ struct DecodeArgs {
   // combines the splits and writes O / lse.  tickets: [B][Hkv], zero on entry and exit.
   unsigned* tickets;
   int out_f16;                  // output dtype: 1 fp16, 0 bf16
-  void* o; long long o_sb, o_sh;
-  float* lse;                   // nullable [B][Hq]
+  void* o; long long o_sb, o_sh, o_ss;
+  float* lse;                   // nullable [B][Hq][Sq]
 };
 cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t stream, int* launches);
 int decode_stage_keys(int G, int D);
-int decode_fused_max_splits(int G, int D);   // largest split count the fused combine can stage
+int decode_fused_max_splits(int rows, int D);   // largest split count the fused combine can stage
 
 // ------------------------------------------------------------ combine (Eq. 8)
 struct CombineArgs {

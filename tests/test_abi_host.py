@@ -86,10 +86,10 @@ def test_alignment_errors(lib):
 
 
 def test_decode_errors(lib):
-    p = _prob(seqlen_q=2)
+    p = _prob(seqlen_q=2)    # multi-token decode (G * Sq = 4 rows) is supported: here it needs workspace
     nul = AttnTensor(None, 0, 0, 0)
     st = lib.attn_splitkv_decode(ctypes.byref(p), _t(), _t(), _t(), 0, None, 0, None, _t(), None, None)
-    assert st == _ffi.ATTN_ERR_UNSUPPORTED
+    assert st == _ffi.ATTN_ERR_WORKSPACE_TOO_SMALL
     p = _prob(seqlen_q=1)
     st = lib.attn_splitkv_decode(ctypes.byref(p), _t(), _t(), _t(), 0, None, 0, None, nul, None, None)
     assert st == _ffi.ATTN_ERR_INVALID_ARGUMENT          # neither parts nor o
@@ -98,9 +98,16 @@ def test_decode_errors(lib):
     parts = AttnParts(FAKE, FAKE, FAKE, 3, 0, 0, 0, 0, 0, 0)
     st = lib.attn_splitkv_decode(ctypes.byref(p), _t(), _t(), _t(), 4, None, 0, ctypes.byref(parts), nul, None, None)
     assert st == _ffi.ATTN_ERR_INVALID_ARGUMENT          # num_parts != splits
-    p = _prob(seqlen_q=1, heads_q=32, heads_kv=2)
+    p = _prob(seqlen_q=1, heads_q=32, heads_kv=1)
     st = lib.attn_splitkv_decode(ctypes.byref(p), _t(), _t(), _t(), 0, None, 0, None, _t(), None, None)
-    assert st == _ffi.ATTN_ERR_UNSUPPORTED              # group of 16 > 8
+    assert st == _ffi.ATTN_ERR_UNSUPPORTED              # group of 32 rows > one 16-row tile
+    p = _prob(seqlen_q=5, heads_q=8, heads_kv=2)
+    st = lib.attn_splitkv_decode(ctypes.byref(p), _t(), _t(), _t(), 0, None, 0, None, _t(), None, None)
+    assert st == _ffi.ATTN_ERR_UNSUPPORTED              # G * seqlen_q = 20 > 16
+    p = _prob(seqlen_q=2, heads_q=8, heads_kv=2)
+    parts = AttnParts(FAKE, FAKE, FAKE, 1, 0, 0, 0, 0, 0, 0)
+    st = lib.attn_splitkv_decode(ctypes.byref(p), _t(), _t(), _t(), 1, None, 0, ctypes.byref(parts), _t(), None, None)
+    assert st == _ffi.ATTN_ERR_UNSUPPORTED              # raw triples only for seqlen_q == 1
 
 
 def test_workspace_and_splits_are_host_functions(lib):

@@ -353,6 +353,38 @@ def test_decode_fused_combine(case):
     assert (o2.float() - outs[0].float()).abs().max().item() <= 2 ** -7
 
 
+MULTI_CASES = [   # (B, Hq, Hkv, Sq, Skv, D, variant, dtype)
+    (2, 8, 2, 2, 1000, 128, dict(causal=True), "bf16"),                 # G*Sq = 8: low mma rows only
+    (2, 8, 2, 4, 1000, 128, dict(causal=True), "bf16"),                 # 16 rows: both row halves
+    (1, 4, 4, 16, 777, 128, dict(causal=True), "bf16"),                 # MHA, 16 queries
+    (1, 16, 2, 2, 600, 64, dict(causal=True, alibi=True), "bf16"),      # G = 8, D = 64
+    (1, 8, 2, 3, 900, 128, dict(causal=True, window_left=300), "f16"),  # 12 rows, window, fp16
+    (1, 16, 1, 1, 500, 128, dict(softcap=2.0), "bf16"),                 # G = 16 single query
+]
+
+
+@pytest.mark.parametrize("case", range(len(MULTI_CASES)))
+def test_decode_multi_token(case):
+    """NEXT-2 small s_q: the G * s_q (head, query) rows of a KV group packed into one
+    16-row mma tile of the split-KV decode kernel, per-row causal masks, fused combine."""
+    B, Hq, Hkv, Sq, Skv, D, var, dt = MULTI_CASES[case]
+    var = dict(var)
+    if var.pop("alibi", False):
+        var["alibi_slopes"] = datagen.alibi_slopes(Hq)
+    p = problem(B, Hq, Hkv, Sq, Skv, D, **var)
+    raw, f64 = gen_qkv(1700 + case, B, Hq, Hkv, Sq, Skv, D, dtype=dt)
+    ref_o, ref_l = oracle.attention(p, *f64)
+    q, k, v = (dgd.to_device(x, dtype=dt) for x in raw)
+    for splits in (0, 3):
+        o, lse = pb.splitkv_decode(q, k, v, num_splits=splits, return_lse=True, **_kw_from(p))
+        torch.cuda.synchronize()
+        assert pb.last_launch_count() == 1
+        assert o.shape == q.shape
+        assert_bf16_close(_bf16_np(o), ref_o, f"multi-token decode case {case} splits={splits}")
+        got_l = lse.cpu().numpy().reshape(ref_l.shape)
+        assert_lse_close(got_l, ref_l, LSE_TOL_BF16, f"multi-token decode lse {case}")
+
+
 def test_combine_kernel_matches_oracle():
     """attn_combine alone on oracle-made partials, with empty (-inf) parts and
     an un-normalised acc output merged again (hierarchical, R3)."""
