@@ -44,6 +44,10 @@ WORKLOADS = {
     "var_scaled_dot": (4, 8, 16, 16, 2048, 64, dict()),
     "var_alibi_causal": (4, 8, 16, 16, 2048, 64, dict(causal=True, alibi=True)),
     "var_softcap_causal": (4, 8, 16, 16, 2048, 64, dict(causal=True, softcap=50.0)),
+    # the config-4 family's other combinations (secondary lines; not in the default run)
+    "var_causal": (4, 8, 16, 16, 2048, 64, dict(causal=True)),
+    "var_alibi": (4, 8, 16, 16, 2048, 64, dict(alibi=True)),
+    "var_softcap": (4, 8, 16, 16, 2048, 64, dict(softcap=50.0)),
 }
 
 

@@ -89,6 +89,12 @@ constexpr bool kTraceBuild = true;    // the timeline trace instruments the non-
 constexpr bool kTraceBuild = false;
 #endif
 constexpr bool kToken = ATTN_TOKEN != 0;   // alternate the two softmax warpgroups' exp phases
+#ifndef ATTN_TOKEN64
+#define ATTN_TOKEN64 ATTN_TOKEN
+#endif
+#ifndef ATTN_F32X2_64
+#define ATTN_F32X2_64 0
+#endif
 
 #ifdef ATTN_SOFTMAX_SPIN
 #define WAIT_SM(bar, par) mbar_wait_spin(bar, par)   // softmax waits for S: poll
@@ -123,24 +129,45 @@ __device__ __forceinline__ bool trace_cta() { return blockIdx.x == 5 && blockIdx
 #define TRACE(ev, step) do { } while (0)
 #endif
 
-template <int D>
+#ifndef ATTN_ALIBI_MMA
+#define ATTN_ALIBI_MMA 1
+#endif
+// ALiBi folded into the QK contraction (D = 64, where the tensor core has slack): one
+// extra K = 16 MMA step adds s*c (s = slope / scale split into three 16-bit parts, c = key
+// column in the tile) to S, so the per-element bias costs nothing on the FMA pipe (see
+// score_tile_alibi_mma).  Shared memory for the constant operands: A_ext(+s), A_ext(-s), B_ext.
+#ifndef ATTN_EXT_NOMMA
+#define ATTN_EXT_NOMMA 0   // timing experiment only: skip the extra MMA (wrong results)
+#endif
+template <int D, bool kAlibi>
+__host__ __device__ constexpr bool alibi_mma() { return ATTN_ALIBI_MMA != 0 && kAlibi && D == 64; }
+
+#ifndef ATTN_D64_STAGES
+#define ATTN_D64_STAGES 10
+#endif
+template <int D, bool kExt = false>
 struct Cfg {
   static constexpr int kBoxes = D / 64;           // 64-column (128 B) swizzle atoms per row
   static constexpr int kQTileBytes = BM * D * 2;
   static constexpr int kKVTileBytes = BN * D * 2;
   // P in shared memory at D = 128 only: at D = 64 the tile's MMAs are half as long, the
   // exponentials dominate and the P stores cost more than the decoupling gains (measured).
-  static constexpr bool kPS = kPSmem && D == 128;
+#ifndef ATTN_P_SMEM64
+#define ATTN_P_SMEM64 0
+#endif
+  static constexpr bool kPS = D == 128 ? kPSmem : ATTN_P_SMEM64 != 0;
   static constexpr int kPTileBytes = kPS ? BM * BN * 2 : 0;
 #ifdef ATTN_TRACE
   static constexpr int kStages = kPS ? 3 : ((D == 128) ? 4 : 8);   // room for the trace
 #else
-  static constexpr int kStages = kPS ? 3 : ((D == 128) ? 5 : 10);
+  static constexpr int kStages = kPS ? ((D == 128) ? 3 : 6) : ((D == 128) ? 5 : (kExt ? 8 : ATTN_D64_STAGES));
 #endif
   // Load-group barriers (ring).  The producer can be at most kStages/2 groups
   // ahead of the issuer's wait, so kStages/2 + 1 barriers never alias a phase.
   static constexpr int kPairBars = kStages / 2 + 1;
-  static constexpr int kSmemQ = 2 * kQTileBytes + 2 * kPTileBytes;   // Q tiles, then P tiles
+  static constexpr int kExtTileBytes = BM * 128;                     // one 128-B swizzle atom wide
+  static constexpr int kExtBytes = kExt ? 3 * kExtTileBytes : 0;     // A_ext(+s), A_ext(-s), B_ext
+  static constexpr int kSmemQ = 2 * kQTileBytes + 2 * kPTileBytes + kExtBytes;   // Q, P, ext tiles
   static constexpr int kSmemKV = kStages * kKVTileBytes;
   static constexpr int kNumBars = 1 + 2 * kStages + 6;
   static constexpr int kXchgBytes = kHalves > 1 ? 2 * kHalves * BM * 4 : 0;   // [tile][half][row] floats
@@ -206,6 +233,18 @@ __device__ __forceinline__ float ex2_poly(float x) {
 
 __device__ __forceinline__ bool active(const Range& r, int j) { return j >= r.lo && j < r.hi; }
 
+// ALiBi-in-MMA class of (query tile starting at row i0, KV tile j): +1 if every key is at or
+// before every query of the tile (bias = -slope (qpos - kpos) = slope*c + a row constant:
+// A_ext(+s)), -1 if every key is at or after every query (A_ext(-s)), 0 mixed (A_ext(+s) and
+// a per-element fix-up).  The issuer and the softmax threads classify identically.
+__device__ __forceinline__ int ext_class(const Shape& s, const VariantParams& v, int i0, int j) {
+  const long long qf = v.q_off + i0, ql = v.q_off + min(i0 + BM, s.Sq) - 1;
+  const long long k0 = v.kv_off + (long long)j * BN, k1 = k0 + BN - 1;
+  if (k1 <= qf) return 1;
+  if (k0 >= ql) return -1;
+  return 0;
+}
+
 __device__ __forceinline__ float u2f(uint32_t u) { return __uint_as_float(u); }
 __device__ __forceinline__ uint32_t f2u(float f) { return __float_as_uint(f); }
 
@@ -244,14 +283,32 @@ __device__ __forceinline__ float score_tile(float (&x)[N], const VariantParams& 
   return mt;
 }
 
+// Mixed ALiBi-in-MMA tile (ext_class 0, built with A_ext(+s)): S = q.k + s c, so
+// x = scale S - slope (c + |qpos - kpos|) = scale S - slope max(dq0, 2c - dq0) (log2 units).
+template <bool kMask, int N>
+__device__ __forceinline__ float score_tile_ext_mixed(float (&x)[N], const VariantParams& v, float nslope2, float dq0,
+                                                      int rel_lo, int rel_hi) {
+  float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    float xv = fmaf(nslope2, fmaxf(dq0, 2.f * (float)c - dq0), x[c] * v.scale_log2);
+    if constexpr (kMask) xv = (c >= rel_lo && c <= rel_hi) ? xv : -INFINITY;
+    x[c] = xv;
+    mx[c & 3] = fmaxf(mx[c & 3], xv);
+  }
+  return fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+}
+
 template <int D, bool kAlibi, bool kSoftcap, bool kF16>
 __global__ void __launch_bounds__(kThreads, 1)
     fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o, const Shape s,
                   const VariantParams v, float* __restrict__ lse) {
-  using C = Cfg<D>;
+  constexpr bool kExt = alibi_mma<D, kAlibi && !kSoftcap>();   // softcap: the bias follows the tanh
+  using C = Cfg<D, kExt>;
   constexpr bool kPSmem = C::kPS;   // shadows the global switch: per head dim
-  constexpr bool kF32x2 = ::attn::kF32x2 && D == 128;   // measured: +1.5-2 % at D = 128, -4 % at D = 64
+  constexpr bool kF32x2 = D == 128 ? ::attn::kF32x2 : ATTN_F32X2_64 != 0;   // measured: +1.5-2 % at D = 128, -4 % at D = 64
+  constexpr bool kToken = D == 128 ? ::attn::kToken : ATTN_TOKEN64 != 0;
   constexpr bool kPlain = !kAlibi && !kSoftcap;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // The 128-byte swizzle needs 1024-byte aligned tiles; dynamic shared memory
@@ -260,6 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = smem_raw;
   uint8_t* sQ = smem;
   uint8_t* sP = smem + 2 * C::kQTileBytes;   // kPSmem: P_t, K-major SW128 [key atom][row][128 B]
+  uint8_t* sExt = smem + 2 * C::kQTileBytes + 2 * C::kPTileBytes;   // kExt: A_ext(+s), A_ext(-s), B_ext
   uint8_t* sKV = smem + C::kSmemQ;
   float* xchg = reinterpret_cast<float*>(sKV + C::kSmemKV);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::kSmemKV + C::kXchgBytes);
@@ -320,6 +378,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_mbarrier_init();
   }
   if (warp == kWarpAlloc) tmem_alloc<512>(tmem_slot);
+  // ALiBi in the contraction (kExt): is it usable for this head?  (fp16 parts must not overflow.)
+  bool ext_on = false;
+  if constexpr (kExt) {
+    const float sx = v.alibi[hq] / v.scale;
+    ext_on = kF16 ? fabsf(sx) < 256.f : fabsf(sx) < 1e30f;
+    if (ext_on && threadIdx.x < 2 * BM) {
+      // Row r of A_ext(+-s) = (s_hi, s_mid, s_lo, 0, ...): s split into three 16-bit parts;
+      // row c of B_ext = (c, c, c, 0, ...) (c <= 127: exact).  K-major, 128-B swizzle.
+      const int r = threadIdx.x & (BM - 1);
+      uint4 row[2][8];
+      for (int u = 0; u < 2; ++u)
+        for (int ch = 0; ch < 8; ++ch) row[u][ch] = make_uint4(0u, 0u, 0u, 0u);
+      if (threadIdx.x < BM) {
+        const float hi = round16<kF16>(sx), mid = round16<kF16>(sx - hi), lo = round16<kF16>(sx - hi - mid);
+        row[0][0] = make_uint4(pack2<kF16>(hi, mid), pack2<kF16>(lo, 0.f), 0u, 0u);
+        row[1][0] = make_uint4(pack2<kF16>(-hi, -mid), pack2<kF16>(-lo, 0.f), 0u, 0u);
+        for (int u = 0; u < 2; ++u)
+          for (int ch = 0; ch < 8; ++ch)
+            *reinterpret_cast<uint4*>(sExt + u * C::kExtTileBytes + r * 128 + ((ch ^ (r & 7)) << 4)) = row[u][ch];
+      } else {
+        const float c = (float)r;
+        row[0][0] = make_uint4(pack2<kF16>(c, c), pack2<kF16>(c, 0.f), 0u, 0u);
+        for (int ch = 0; ch < 8; ++ch)
+          *reinterpret_cast<uint4*>(sExt + 2 * C::kExtTileBytes + r * 128 + ((ch ^ (r & 7)) << 4)) = row[0][ch];
+      }
+      fence_proxy_async_smem();   // generic-proxy stores -> tensor core reads
+    }
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -411,7 +497,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         WAIT_LM(&kv_full[g % C::kPairBars], (g / C::kPairBars) & 1);
         tc_fence_after();
       };
-      auto qk = [&](int t, int it) {   // S_t = Q_t K^T
+      auto qk = [&](int t, int it, int j) {   // S_t = Q_t K_j^T (+ s*c, ALiBi in the contraction)
         const uint32_t sq = smem_u32(sQ + t * C::kQTileBytes);
         const uint32_t sk = smem_u32(sKV + (it % C::kStages) * C::kKVTileBytes);
 #pragma unroll
@@ -420,6 +506,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t kb = (kk >> 2) * (BN * 128) + (kk & 3) * 32;
           mma_ss_warp(tS[t], smem_desc_sw128(sq + ka, 16, 1024), smem_desc_sw128(sk + kb, 16, 1024), idesc_qk,
                  kk > 0 ? 1u : 0u);
+        }
+        if constexpr (kExt) {
+          if (ext_on && !ATTN_EXT_NOMMA) {
+            const int cls = ext_class(s, v, row0 + t * BM, j);
+            const uint32_t sa = smem_u32(sExt + (cls < 0 ? C::kExtTileBytes : 0));
+            mma_ss_warp(tS[t], smem_desc_sw128(sa, 16, 1024), smem_desc_sw128(smem_u32(sExt + 2 * C::kExtTileBytes), 16, 1024),
+                        idesc_qk, 1u);
+          }
         }
         mma_commit_warp(&s_full[t]);
       };
@@ -447,7 +541,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             named_bar_sync(kBarS0 + t, kTileThreads + 32);
             tc_fence_after();
           }
-          qk(t, it);
+          qk(t, it, i);
         };
         auto pv_p = [&](int t, int it, bool acc) {   // O_t += P_t V (P from shared memory)
           named_bar_sync(kBarP0 + t, kTileThreads + 32);
@@ -499,8 +593,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       } else {
       wait_group(0);
-      if (active(rg[0], ulo)) qk(0, 0);
-      if (active(rg[1], ulo)) qk(1, 0);
+      if (active(rg[0], ulo)) qk(0, 0, ulo);
+      if (active(rg[1], ulo)) qk(1, 0, ulo);
       mma_commit_warp(&kv_empty[0]);
       for (int j = ulo; j < uhi; ++j) {
         const int itV = 2 * (j - ulo) + 1, itK1 = itV + 1;
@@ -509,13 +603,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) TRACE(12, j);
         if (active(rg[0], j)) pv(0, itV, j > rg[0].lo);
         if (lane == 0) TRACE(0, j);
-        if (more && active(rg[0], j + 1)) qk(0, itK1);
+        if (more && active(rg[0], j + 1)) qk(0, itK1, j + 1);
         if (lane == 0) TRACE(1, j);
         if (active(rg[1], j)) pv(1, itV, j > rg[1].lo);
         if (lane == 0) TRACE(2, j);
         mma_commit_warp(&kv_empty[itV % C::kStages]);
         if (more) {
-          if (active(rg[1], j + 1)) qk(1, itK1);
+          if (active(rg[1], j + 1)) qk(1, itK1, j + 1);
           mma_commit_warp(&kv_empty[itK1 % C::kStages]);
         }
       }
@@ -582,8 +676,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool need_mask = !(j * BN >= R.jlo_last && (j + 1) * BN - 1 <= R.jhi_first);
       const int rel_lo = jlo_row - j * BN - c_base, rel_hi = jhi_row - j * BN - c_base;
       const float dq0 = (float)(qpos - v.kv_off - (long long)j * BN - c_base);
-      float mt = need_mask ? score_tile<kAlibi, kSoftcap, true>(x, v, nslope2, dq0, rel_lo, rel_hi)
-                           : score_tile<kAlibi, kSoftcap, false>(x, v, nslope2, dq0, rel_lo, rel_hi);
+      // exponent argument a = x * e_mul + e_off' (e_off' = e_off - m, set after the max)
+      float e_mul = kPlain ? v.scale_log2 : 1.f, e_off = 0.f;
+      float mt;
+      if (kExt && ext_on) {
+        // ALiBi in the contraction: S already holds q.k + (+-s) c (see ext_class)
+        const int cls = ext_class(s, v, row0 + t * BM, j);
+        if (cls != 0) {   // bias = row constant: the plain path with an offset
+          e_mul = v.scale_log2;
+          e_off = (cls > 0 ? nslope2 : -nslope2) * dq0;
+          mt = (need_mask ? score_tile<false, false, true>(x, v, nslope2, dq0, rel_lo, rel_hi)
+                          : score_tile<false, false, false>(x, v, nslope2, dq0, rel_lo, rel_hi)) + e_off;
+        } else {
+          mt = need_mask ? score_tile_ext_mixed<true>(x, v, nslope2, dq0, rel_lo, rel_hi)
+                         : score_tile_ext_mixed<false>(x, v, nslope2, dq0, rel_lo, rel_hi);
+        }
+      } else {
+        mt = need_mask ? score_tile<kAlibi, kSoftcap, true>(x, v, nslope2, dq0, rel_lo, rel_hi)
+                       : score_tile<kAlibi, kSoftcap, false>(x, v, nslope2, dq0, rel_lo, rel_hi);
+      }
       if constexpr (kHalves > 1) {
         // both halves must have loaded S before either overwrites it with P (P aliases S)
         *my_x = mt;
@@ -621,6 +732,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
       }
       if (tid_t == 0) TRACE(6 + 4 * t, j);
+      const float e_add = e_off - m_use_t;
       float sum0 = 0.f, sum1 = 0.f;
 #pragma unroll
       for (int c0 = 0; c0 < kHC; c0 += 32) {
@@ -628,8 +740,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           float a0, a1;
-          if constexpr (kF32x2) {
+          if constexpr (kF32x2 && kExt) {
+            fma2_bc(a0, a1, x[c0 + 2 * e], x[c0 + 2 * e + 1], e_mul, e_add);
+          } else if constexpr (kF32x2) {
             fma2_bc(a0, a1, x[c0 + 2 * e], x[c0 + 2 * e + 1], kPlain ? v.scale_log2 : 1.f, -m_use_t);
+          } else if constexpr (kExt) {
+            a0 = fmaf(x[c0 + 2 * e], e_mul, e_add);
+            a1 = fmaf(x[c0 + 2 * e + 1], e_mul, e_add);
           } else if constexpr (kPlain) {
             a0 = fmaf(x[c0 + 2 * e], v.scale_log2, -m_use_t);
             a1 = fmaf(x[c0 + 2 * e + 1], v.scale_log2, -m_use_t);
@@ -1221,7 +1338,7 @@ cudaError_t launch_persist(const FwdTcArgs& a, cudaStream_t stream) {
 
 template <int D, bool kAlibi, bool kSoftcap, bool kF16>
 cudaError_t launch_t(const FwdTcArgs& a, cudaStream_t stream) {
-  using C = Cfg<D>;
+  using C = Cfg<D, alibi_mma<D, kAlibi && !kSoftcap>()>;
   if constexpr (D == 128 && C::kPS && kHalves == 1 && !kTraceBuild) {
     const bool pure_causal = a.v.causal && a.v.window_left < 0 && a.v.window_right < 0;
     if (ATTN_PERSIST == 2 || (ATTN_PERSIST == 1 && pure_causal)) return launch_persist<kAlibi, kSoftcap, kF16>(a, stream);

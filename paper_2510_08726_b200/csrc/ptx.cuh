@@ -327,5 +327,17 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   if constexpr (kF16) return pack_f16x2(lo, hi);
   else return pack_bf16x2(lo, hi);
 }
+// x rounded (RNE) to the kernel's 16-bit element type, as a float.
+template <bool kF16>
+__device__ __forceinline__ float round16(float x) {
+  const uint32_t u = pack2<kF16>(x, 0.f) & 0xFFFFu;
+  if constexpr (kF16) {
+    float f;
+    asm("{ .reg .f16 h; mov.b16 h, %1; cvt.f32.f16 %0, h; }" : "=f"(f) : "h"((unsigned short)u));
+    return f;
+  } else {
+    return __uint_as_float(u << 16);
+  }
+}
 
 }  // namespace attn

@@ -89,6 +89,10 @@ VARIANTS = {
     "alibi_causal": dict(causal=True, alibi=True),
     "softcap_causal": dict(causal=True, softcap=2.0),
     "alibi_softcap": dict(alibi=True, softcap=2.0, window_left=200, window_right=0),
+    # D = 64 folds ALiBi into the QK contraction: tiles wholly below, wholly above and across
+    # the diagonal take different paths (fwd_tc.cu ext_class)
+    "alibi": dict(alibi=True),
+    "alibi_band": dict(alibi=True, window_left=150, window_right=21),
 }
 
 
@@ -119,13 +123,31 @@ def test_bf16_prefill_small(name, D):
     (129, 129, dict()),
 ])
 def test_bf16_prefill_rectangular(Sq, Skv, extra):
-    B, Hq, Hkv, D = 1, 2, 1, 128
+    _rectangular(Sq, Skv, extra, 128)
+
+
+@pytest.mark.parametrize("Sq,Skv,extra", [
+    (130, 1000, dict(q_pos_offset=400)),                                   # keys on both sides, non-causal
+    (257, 300, dict(causal=True, kv_pos_offset=100, seqlen_kv_total=400)), # KV shard of a longer sequence
+    (100, 700, dict(causal=True)),                                         # chunked prefill, bottom-right
+    (300, 900, dict(window_left=70, window_right=300, q_pos_offset=250)),  # band crossing tile edges
+    (200, 600, dict(scale=1e-3)),                                          # |slope / scale| = 707: large ALiBi term
+])
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+def test_alibi_d64_rectangular(Sq, Skv, extra, dtype):
+    """ALiBi at D = 64 (bias folded into the QK contraction; fp16 with |s| >= 256 falls back)."""
+    _rectangular(Sq, Skv, dict(extra, alibi_slopes=datagen.alibi_slopes(4)), 64, Hq=4, Hkv=2, dtype=dtype)
+
+
+def _rectangular(Sq, Skv, extra, D, Hq=2, Hkv=1, dtype="bf16"):
+    B = 1
     p = problem(B, Hq, Hkv, Sq, Skv, D, **extra)
-    raw, f64 = gen_qkv(1000 + Sq + Skv, B, Hq, Hkv, Sq, Skv, D)
+    gdt = "f16" if dtype == "fp16" else "bf16"
+    raw, f64 = gen_qkv(1000 + Sq + Skv + D, B, Hq, Hkv, Sq, Skv, D, gdt)
     ref_o, ref_l = oracle.attention(p, *f64)
-    q, k, v = (dgd.to_device(x) for x in raw)
+    q, k, v = (dgd.to_device(x, dtype=gdt) for x in raw)
     o, lse = pb.fused_fwd(q, k, v, return_lse=True, **_kw_from(p))
-    assert_bf16_close(_bf16_np(o), ref_o, f"Sq={Sq} Skv={Skv} {extra}")
+    assert_bf16_close(_bf16_np(o), ref_o, f"{dtype} D={D} Sq={Sq} Skv={Skv} {extra}")
     assert_lse_close(lse.cpu().numpy(), ref_l, LSE_TOL_BF16, "lse")
 
 
@@ -206,6 +228,7 @@ FULL = {
     "gqa_window": dict(cid=3, B=4, Hq=32, Hkv=8, S=8192, D=128, causal=True, window_left=4095),
     "variants_scaled_dot": dict(cid=4, B=8, Hq=16, Hkv=16, S=2048, D=64),
     "variants_alibi_causal": dict(cid=4, B=8, Hq=16, Hkv=16, S=2048, D=64, causal=True, alibi=True),
+    "variants_alibi": dict(cid=4, B=8, Hq=16, Hkv=16, S=2048, D=64, alibi=True),
     "variants_softcap_causal": dict(cid=4, B=8, Hq=16, Hkv=16, S=2048, D=64, causal=True, softcap=2.0),
 }
 
@@ -450,7 +473,7 @@ def test_device_generator_fp16_is_bit_identical():
 
 
 @pytest.mark.parametrize("D", [128, 64])
-@pytest.mark.parametrize("name", ["global", "causal", "alibi_causal", "softcap_causal", "window_band"])
+@pytest.mark.parametrize("name", ["global", "causal", "alibi_causal", "softcap_causal", "window_band", "alibi"])
 def test_fp16_prefill_small(name, D):
     kw = dict(VARIANTS[name])
     B, Hq, Hkv, S = 1, 4, 2, 300

@@ -13,7 +13,7 @@ from paper_2510_08726_b200 import _ffi
 _ffi.load(lib_path)
 import paper_2510_08726_b200 as pb
 from datagen import device as dgd
-B, H, S, D = 8, 16, 4096, 128
+B, H, S, D = (int(x) for x in os.environ.get("TRACE_CFG", "8,16,4096,128").split(","))
 q, k, v = (dgd.tensor(1, i, (B, H, S, D)) for i in (1, 2, 3))
 causal = len(sys.argv) > 1 and sys.argv[1] == "causal"
 for _ in range(3):
@@ -25,5 +25,5 @@ t0 = tr[3, 0]
 names = {12: "mma:V ready", 13: "mma:P0 seen", 15: "mma:K+1 ready", 14: "mma:P1 seen", 0: "mma:PV0 iss", 1: "mma:QK0+1 iss", 2: "mma:PV1 iss", 4: "sm0:wait S", 5: "sm0:S ready",
          6: "sm0:token", 7: "sm0:P done", 8: "sm1:wait S", 9: "sm1:S ready", 10: "sm1:token", 11: "sm1:P done", 16: "w4 exp end", 17: "w5 exp end", 18: "w6 exp end", 19: "w7 exp end", 20: "w4 arrive", 21: "w5 arrive", 22: "w6 arrive", 23: "w7 arrive", 24: "ld:K issue", 25: "ld:V issue"}
 print("step " + " ".join(f"{names[e]:>13s}" for e in names))
-for j in range(33):
+for j in range(min(33, S // 128 + 1)):
     print(f"{j:4d} " + " ".join(f"{((tr[e, j] - t0) & 0xffffffff) if tr[e, j] else 0:13d}" for e in names))
