@@ -257,28 +257,69 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       : "memory");
 }
 
+// Max-pass over one S row held in registers, in chunks of 32 columns: `xf(xv, c)` applies
+// score_mod; on mask tiles each chunk is classified warp-uniformly (all 32 rows of the warp
+// see it wholly allowed / wholly masked / partial) so only partial chunks pay the per-element
+// compare-and-select (on a causal diagonal tile that is one chunk in four per warp).
+#ifndef ATTN_CHUNK_MASK
+#define ATTN_CHUNK_MASK 1
+#endif
+// (kChunked = false: every element of a mask tile is compared; measured better at D = 64,
+// where the chunk branches cost registers in the MUFU-bound kernels.)
+template <bool kMask, bool kChunked, int N, class XF>
+__device__ __forceinline__ float row_max_pass(float (&x)[N], int rel_lo, int rel_hi, XF xf) {
+  float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};   // independent chains for ILP
+  if constexpr (!kChunked) {
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      float xv = xf(x[c], c);
+      if constexpr (kMask) xv = (c >= rel_lo && c <= rel_hi) ? xv : -INFINITY;
+      x[c] = xv;
+      mx[c & 3] = fmaxf(mx[c & 3], xv);
+    }
+  } else {
+#pragma unroll
+  for (int q = 0; q < N / 32; ++q) {
+    bool part = false;   // some row of the warp has a masked column in this chunk
+    if constexpr (kMask) part = !__all_sync(0xffffffffu, rel_lo <= q * 32 && rel_hi >= q * 32 + 31);
+    if (!part) {
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        const int c = q * 32 + e;
+        const float xv = xf(x[c], c);
+        x[c] = xv;
+        mx[c & 3] = fmaxf(mx[c & 3], xv);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        const int c = q * 32 + e;
+        const float xv = (c >= rel_lo && c <= rel_hi) ? xf(x[c], c) : -INFINITY;
+        x[c] = xv;
+        mx[c & 3] = fmaxf(mx[c & 3], xv);
+      }
+    }
+  }
+  }
+  return fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+}
+
 // score_mod + mask of one S row (BN raw fp32 dots in `x`), in place, into the
 // log2 domain used by the exponentials; returns the row max of the tile.
 // Plain variant: x stays raw (scale folded into the exp FFMA) and the max is
 // rescaled afterwards (scale > 0 so max commutes with it).
-template <bool kAlibi, bool kSoftcap, bool kMask, int N>
+template <bool kAlibi, bool kSoftcap, bool kMask, bool kChunked = true, int N>
 __device__ __forceinline__ float score_tile(float (&x)[N], const VariantParams& v, float nslope2, float dq0,
                                             int rel_lo, int rel_hi) {
-  float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};   // independent chains for ILP
-#pragma unroll
-  for (int c = 0; c < N; ++c) {
-    float xv = x[c];
+  float mt = row_max_pass<kMask, kChunked>(x, rel_lo, rel_hi, [&](float xv, int c) {
     if constexpr (kSoftcap) {
       xv = v.softcap_log2 * tanh_approx(xv * v.scale_over_cap);   // R3: cap * tanh(x / cap)
     } else if constexpr (kAlibi) {
       xv = xv * v.scale_log2;
     }
     if constexpr (kAlibi) xv = fmaf(nslope2, fabsf(dq0 - (float)c), xv);  // R4: -slope |qpos - kpos|
-    if constexpr (kMask) xv = (c >= rel_lo && c <= rel_hi) ? xv : -INFINITY;
-    x[c] = xv;
-    mx[c & 3] = fmaxf(mx[c & 3], xv);
-  }
-  float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+    return xv;
+  });
   if constexpr (!kAlibi && !kSoftcap) mt *= v.scale_log2;
   return mt;
 }
@@ -288,15 +329,9 @@ __device__ __forceinline__ float score_tile(float (&x)[N], const VariantParams& 
 template <bool kMask, int N>
 __device__ __forceinline__ float score_tile_ext_mixed(float (&x)[N], const VariantParams& v, float nslope2, float dq0,
                                                       int rel_lo, int rel_hi) {
-  float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-  for (int c = 0; c < N; ++c) {
-    float xv = fmaf(nslope2, fmaxf(dq0, 2.f * (float)c - dq0), x[c] * v.scale_log2);
-    if constexpr (kMask) xv = (c >= rel_lo && c <= rel_hi) ? xv : -INFINITY;
-    x[c] = xv;
-    mx[c & 3] = fmaxf(mx[c & 3], xv);
-  }
-  return fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+  return row_max_pass<kMask, false>(x, rel_lo, rel_hi, [&](float xv, int c) {
+    return fmaf(nslope2, fmaxf(dq0, 2.f * (float)c - dq0), xv * v.scale_log2);
+  });
 }
 
 template <int D, bool kAlibi, bool kSoftcap, bool kF16>
@@ -305,6 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o, const Shape s,
                   const VariantParams v, float* __restrict__ lse) {
   constexpr bool kExt = alibi_mma<D, kAlibi && !kSoftcap>();   // softcap: the bias follows the tanh
+  constexpr bool kChunkMask = D == 128 && ATTN_CHUNK_MASK;   // chunk-classified masking (measured: + at D = 128, - at D = 64)
   using C = Cfg<D, kExt>;
   constexpr bool kPSmem = C::kPS;   // shadows the global switch: per head dim
   constexpr bool kF32x2 = D == 128 ? ::attn::kF32x2 : ATTN_F32X2_64 != 0;   // measured: +1.5-2 % at D = 128, -4 % at D = 64
@@ -685,15 +721,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (cls != 0) {   // bias = row constant: the plain path with an offset
           e_mul = v.scale_log2;
           e_off = (cls > 0 ? nslope2 : -nslope2) * dq0;
-          mt = (need_mask ? score_tile<false, false, true>(x, v, nslope2, dq0, rel_lo, rel_hi)
-                          : score_tile<false, false, false>(x, v, nslope2, dq0, rel_lo, rel_hi)) + e_off;
+          mt = (need_mask ? score_tile<false, false, true, kChunkMask>(x, v, nslope2, dq0, rel_lo, rel_hi)
+                          : score_tile<false, false, false, kChunkMask>(x, v, nslope2, dq0, rel_lo, rel_hi)) + e_off;
         } else {
           mt = need_mask ? score_tile_ext_mixed<true>(x, v, nslope2, dq0, rel_lo, rel_hi)
                          : score_tile_ext_mixed<false>(x, v, nslope2, dq0, rel_lo, rel_hi);
         }
       } else {
-        mt = need_mask ? score_tile<kAlibi, kSoftcap, true>(x, v, nslope2, dq0, rel_lo, rel_hi)
-                       : score_tile<kAlibi, kSoftcap, false>(x, v, nslope2, dq0, rel_lo, rel_hi);
+        mt = need_mask ? score_tile<kAlibi, kSoftcap, true, kChunkMask>(x, v, nslope2, dq0, rel_lo, rel_hi)
+                       : score_tile<kAlibi, kSoftcap, false, kChunkMask>(x, v, nslope2, dq0, rel_lo, rel_hi);
       }
       if constexpr (kHalves > 1) {
         // both halves must have loaded S before either overwrites it with P (P aliases S)
@@ -1184,8 +1220,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool need_mask = !(j * BN >= R.jlo_last && (j + 1) * BN - 1 <= R.jhi_first);
         const int rel_lo = jlo_row - j * BN, rel_hi = jhi_row - j * BN;
         const float dq0 = (float)(qpos - v.kv_off - (long long)j * BN);
-        const float mt = need_mask ? score_tile<kAlibi, kSoftcap, true>(x, v, nslope2, dq0, rel_lo, rel_hi)
-                                   : score_tile<kAlibi, kSoftcap, false>(x, v, nslope2, dq0, rel_lo, rel_hi);
+        const float mt = need_mask ? score_tile<kAlibi, kSoftcap, true, ATTN_CHUNK_MASK != 0>(x, v, nslope2, dq0, rel_lo, rel_hi)
+                                   : score_tile<kAlibi, kSoftcap, false, ATTN_CHUNK_MASK != 0>(x, v, nslope2, dq0, rel_lo, rel_hi);
         const float m_run = fmaxf(m_ref, mt);
         bool move, need_o;
         if (m_ref == -INFINITY) {
