@@ -307,6 +307,24 @@ def main_gpu(args):
                      "kernel": "fwd_tc_kernel (tcgen05 Rolling Update)",
                      "algorithmic_flops_per_launch": flops},
     }
+    # The exponentials (and softcap's tanh) run on the SFU (MUFU): 16 results/clk/SM (measured,
+    # profiles/r1_microbench.md).  At D = 128 a 128x128 tile's exponentials take exactly as long
+    # as its two MMAs; at D = 64 twice as long, so the D = 64 lines are bound by MUFU ("alu"),
+    # not by the tensor core.  MUFU work = one ex2 per allowed (q, k) pair (+ one tanh with softcap).
+    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+    sm_mhz = float((clocks or {}).get("sm_max_mhz") or 1965.0)
+    mufu_ops = allowed_pairs(S, var) * B * Hq * (2 if var.get("softcap") else 1)
+    mufu_peak = 16.0 * sm_count * sm_mhz * 1e6 / 1e9                      # Gop/s
+    mufu_ach = mufu_ops / (ms * 1e-3) / 1e9
+    mufu = {"bound": "alu", "achieved": mufu_ach, "peak": mufu_peak, "unit": "Gop/s (MUFU ex2/tanh)",
+            "frac": mufu_ach / mufu_peak, "ops_per_launch": mufu_ops,
+            "peak_src": f"16 MUFU results/clk/SM x {sm_count} SMs x {sm_mhz:.0f} MHz"}
+    if D == 64:
+        tensor = line["roofline"]
+        line["roofline"] = dict(mufu, traffic=traffic, kernel=tensor["kernel"],
+                                tensor={k: tensor[k] for k in ("achieved", "peak", "unit", "frac")})
+    else:
+        line["roofline"]["mufu"] = mufu
 
     # ------------------------------------------------------------- e2e through the public API, host buffers
     if not args.no_e2e:

@@ -51,8 +51,21 @@ constexpr int BN = 128;
 constexpr int kHalves = ATTN_ROW_SPLIT;
 constexpr int kTileThreads = 128 * kHalves;            // softmax threads per query tile
 constexpr int kSoftmaxWarps = 2 * kTileThreads / 32;
+#ifndef ATTN_REGS
+#define ATTN_REGS 0   // measured (same box): 216 removes the D = 128 spills but is 1.5-4 % slower
+#endif
+// Register budget.  The register file is split across the 4 SM sub-partitions (warp w runs on
+// w % 4, 16 K registers each), so with 10-12 warps three share a sub-partition and each gets
+// at most 168 registers -- too few for a softmax thread holding its 128-column S row (spills in
+// the exponential loop).  ATTN_REGS > 0: the CTA is 3 warpgroups (12 warps: softmax tile 0,
+// softmax tile 1, then producer / MMA / TMEM allocator / idle) and after the prologue the
+// softmax warpgroups raise their budget to ATTN_REGS with setmaxnreg while the third
+// warpgroup drops to 504 - 2 * ATTN_REGS: the pool is what the CTA got at launch,
+// 168 x 384 = 12 warps x 32 x (2 x 224 + 56) / 3 (an increase the pool cannot serve blocks forever).
+constexpr int kRegsSoftmax = ATTN_REGS, kRegsOther = ATTN_REGS ? 504 - 2 * ATTN_REGS : 0;
+static_assert(ATTN_REGS == 0 || (kRegsOther >= 24 && kRegsOther % 8 == 0 && kRegsSoftmax % 8 == 0), "setmaxnreg");
 constexpr int kWarpLoad = kSoftmaxWarps, kWarpMma = kSoftmaxWarps + 1, kWarpAlloc = kSoftmaxWarps + 2;
-constexpr int kThreads = (kSoftmaxWarps + 3) * 32;
+constexpr int kThreads = (kSoftmaxWarps + (ATTN_REGS ? 4 : 3)) * 32;
 constexpr int kHC = BN / kHalves;                       // S columns per softmax thread
 #ifndef ATTN_PREFETCH
 #define ATTN_PREFETCH 0
@@ -448,6 +461,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) TRACE(3, 0);
 
+  if (warp >= kSoftmaxWarps) {   // warpgroup 2: producer, MMA issuer, TMEM allocator, idle
+  if constexpr (kRegsOther > 0) reg_dealloc<kRegsOther>();
   if (warp == kWarpLoad) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
@@ -651,7 +666,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       }
     }
-  } else if (warp < kSoftmaxWarps) {
+  }
+  } else {   // warpgroups 0 and 1: softmax of query tiles 0 and 1
+  if constexpr (kRegsSoftmax > 0) reg_alloc<kRegsSoftmax>();
     // ------------------------------------------------------------ softmax / correction / epilogue
     // Thread (tile t, row r, column half h) owns S columns [h*kHC, (h+1)*kHC) of row r.
     const int t = (int)warp / (kSoftmaxWarps / 2);
@@ -1051,6 +1068,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  if (warp >= kSoftmaxWarps) {   // warpgroup 2: producer, MMA issuer, TMEM allocator, idle
+  if constexpr (kRegsOther > 0) reg_dealloc<kRegsOther>();
   if (warp == kWarpLoad) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
@@ -1178,7 +1197,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int t = 0; t < 2; ++t)      // the softmax's arrival for its last S load
       if (qk_any[t]) named_bar_sync(kBarS0 + t, kTileThreads + 32);
-  } else if (warp < kSoftmaxWarps) {
+  }
+  } else {   // warpgroups 0 and 1: softmax of query tiles 0 and 1
+  if constexpr (kRegsSoftmax > 0) reg_alloc<kRegsSoftmax>();
     // ------------------------------------------------------------ softmax / correction / epilogue
     const int t = (int)warp / 4;
     const int wq = warp & 3;
