@@ -51,21 +51,8 @@ constexpr int BN = 128;
 constexpr int kHalves = ATTN_ROW_SPLIT;
 constexpr int kTileThreads = 128 * kHalves;            // softmax threads per query tile
 constexpr int kSoftmaxWarps = 2 * kTileThreads / 32;
-#ifndef ATTN_REGS
-#define ATTN_REGS 0   // measured (same box): 216 removes the D = 128 spills but is 1.5-4 % slower
-#endif
-// Register budget.  The register file is split across the 4 SM sub-partitions (warp w runs on
-// w % 4, 16 K registers each), so with 10-12 warps three share a sub-partition and each gets
-// at most 168 registers -- too few for a softmax thread holding its 128-column S row (spills in
-// the exponential loop).  ATTN_REGS > 0: the CTA is 3 warpgroups (12 warps: softmax tile 0,
-// softmax tile 1, then producer / MMA / TMEM allocator / idle) and after the prologue the
-// softmax warpgroups raise their budget to ATTN_REGS with setmaxnreg while the third
-// warpgroup drops to 504 - 2 * ATTN_REGS: the pool is what the CTA got at launch,
-// 168 x 384 = 12 warps x 32 x (2 x 224 + 56) / 3 (an increase the pool cannot serve blocks forever).
-constexpr int kRegsSoftmax = ATTN_REGS, kRegsOther = ATTN_REGS ? 504 - 2 * ATTN_REGS : 0;
-static_assert(ATTN_REGS == 0 || (kRegsOther >= 24 && kRegsOther % 8 == 0 && kRegsSoftmax % 8 == 0), "setmaxnreg");
 constexpr int kWarpLoad = kSoftmaxWarps, kWarpMma = kSoftmaxWarps + 1, kWarpAlloc = kSoftmaxWarps + 2;
-constexpr int kThreads = (kSoftmaxWarps + (ATTN_REGS ? 4 : 3)) * 32;
+constexpr int kThreads = (kSoftmaxWarps + 3) * 32;
 constexpr int kHC = BN / kHalves;                       // S columns per softmax thread
 #ifndef ATTN_PREFETCH
 #define ATTN_PREFETCH 0
@@ -158,7 +145,20 @@ __host__ __device__ constexpr bool alibi_mma() { return ATTN_ALIBI_MMA != 0 && k
 #ifndef ATTN_D64_STAGES
 #define ATTN_D64_STAGES 10
 #endif
-template <int D, bool kExt = false>
+#ifndef ATTN_NT64
+#define ATTN_NT64 1   // measured (same box): causal D = 64 +5 %, scaled-dot +1 %
+#endif
+#ifndef ATTN_NT1_STAGES64
+#define ATTN_NT1_STAGES64 5
+#endif
+#ifndef ATTN_NT128
+#define ATTN_NT128 2   // NT = 1 at D = 128 (TMEM-aliased P, 2-slot ring): -11 % (MHA)
+#endif
+// NT = query tiles per CTA.  NT = 2: one CTA per SM, its two tiles' exp phases alternate
+// (token).  NT = 1: 128-row CTAs, TWO resident per SM (256 TMEM columns and < 113 KiB of
+// shared memory each, 6 warps): the two CTAs' rolling loops interleave on their own and one
+// CTA's prologue/epilogue overlaps the other's loop.
+template <int D, bool kExt = false, int NT = 2>
 struct Cfg {
   static constexpr int kBoxes = D / 64;           // 64-column (128 B) swizzle atoms per row
   static constexpr int kQTileBytes = BM * D * 2;
@@ -168,19 +168,20 @@ struct Cfg {
 #ifndef ATTN_P_SMEM64
 #define ATTN_P_SMEM64 0
 #endif
-  static constexpr bool kPS = D == 128 ? kPSmem : ATTN_P_SMEM64 != 0;
+  static constexpr bool kPS = NT == 1 ? false : (D == 128 ? kPSmem : ATTN_P_SMEM64 != 0);
   static constexpr int kPTileBytes = kPS ? BM * BN * 2 : 0;
 #ifdef ATTN_TRACE
   static constexpr int kStages = kPS ? 3 : ((D == 128) ? 4 : 8);   // room for the trace
 #else
-  static constexpr int kStages = kPS ? ((D == 128) ? 3 : 6) : ((D == 128) ? 5 : (kExt ? 8 : ATTN_D64_STAGES));
+  static constexpr int kStages = NT == 1 ? ((D == 128) ? 2 : (kExt ? 3 : ATTN_NT1_STAGES64))
+                                          : kPS ? ((D == 128) ? 3 : 6) : ((D == 128) ? 5 : (kExt ? 8 : ATTN_D64_STAGES));
 #endif
   // Load-group barriers (ring).  The producer can be at most kStages/2 groups
   // ahead of the issuer's wait, so kStages/2 + 1 barriers never alias a phase.
   static constexpr int kPairBars = kStages / 2 + 1;
   static constexpr int kExtTileBytes = BM * 128;                     // one 128-B swizzle atom wide
   static constexpr int kExtBytes = kExt ? 3 * kExtTileBytes : 0;     // A_ext(+s), A_ext(-s), B_ext
-  static constexpr int kSmemQ = 2 * kQTileBytes + 2 * kPTileBytes + kExtBytes;   // Q, P, ext tiles
+  static constexpr int kSmemQ = NT * kQTileBytes + NT * kPTileBytes + kExtBytes;   // Q, P, ext tiles
   static constexpr int kSmemKV = kStages * kKVTileBytes;
   static constexpr int kNumBars = 1 + 2 * kStages + 6;
   static constexpr int kXchgBytes = kHalves > 1 ? 2 * kHalves * BM * 4 : 0;   // [tile][half][row] floats
@@ -347,17 +348,32 @@ __device__ __forceinline__ float score_tile_ext_mixed(float (&x)[N], const Varia
   });
 }
 
-template <int D, bool kAlibi, bool kSoftcap, bool kF16>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int NT>
+struct Roles {   // warp roles of fwd_tc_kernel (kHalves == 1 for NT == 1)
+  static constexpr int kSoftmaxWarps = NT * kTileThreads / 32;
+  static constexpr int kWarpLoad = kSoftmaxWarps, kWarpMma = kSoftmaxWarps + 1;
+  static constexpr int kWarpAlloc = NT == 2 ? kSoftmaxWarps + 2 : kWarpMma;   // NT = 1: the MMA warp allocates
+  static constexpr int kThreads = (NT == 2 ? kSoftmaxWarps + 3 : kSoftmaxWarps + 2) * 32;
+  static constexpr int kMinBlocks = NT == 2 ? 1 : 2;
+  static constexpr int kTmemCols = NT == 2 ? 512 : 256;
+  static constexpr uint32_t kOBase = NT == 2 ? 256 : 128;   // TMEM column of O_0 (S_t at t * 128)
+};
+static_assert(kHalves == 1 || (ATTN_NT64 == 2 && ATTN_NT128 == 2), "NT = 1 needs one thread per row");
+
+template <int D, bool kAlibi, bool kSoftcap, bool kF16, int NT>
+__global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
     fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o, const Shape s,
                   const VariantParams v, float* __restrict__ lse) {
   constexpr bool kExt = alibi_mma<D, kAlibi && !kSoftcap>();   // softcap: the bias follows the tanh
   constexpr bool kChunkMask = D == 128 && ATTN_CHUNK_MASK;   // chunk-classified masking (measured: + at D = 128, - at D = 64)
-  using C = Cfg<D, kExt>;
+  using C = Cfg<D, kExt, NT>;
+  using Ro = Roles<NT>;
+  constexpr int kSoftmaxWarps = Ro::kSoftmaxWarps, kWarpLoad = Ro::kWarpLoad, kWarpMma = Ro::kWarpMma;
+  constexpr int kWarpAlloc = Ro::kWarpAlloc;
   constexpr bool kPSmem = C::kPS;   // shadows the global switch: per head dim
   constexpr bool kF32x2 = D == 128 ? ::attn::kF32x2 : ATTN_F32X2_64 != 0;   // measured: +1.5-2 % at D = 128, -4 % at D = 64
-  constexpr bool kToken = D == 128 ? ::attn::kToken : ATTN_TOKEN64 != 0;
+  constexpr bool kToken = NT == 2 && (D == 128 ? ::attn::kToken : ATTN_TOKEN64 != 0);
   constexpr bool kPlain = !kAlibi && !kSoftcap;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // The 128-byte swizzle needs 1024-byte aligned tiles; dynamic shared memory
@@ -365,8 +381,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if ((smem_u32(smem_raw) & 1023) != 0) __trap();
   uint8_t* smem = smem_raw;
   uint8_t* sQ = smem;
-  uint8_t* sP = smem + 2 * C::kQTileBytes;   // kPSmem: P_t, K-major SW128 [key atom][row][128 B]
-  uint8_t* sExt = smem + 2 * C::kQTileBytes + 2 * C::kPTileBytes;   // kExt: A_ext(+s), A_ext(-s), B_ext
+  uint8_t* sP = smem + NT * C::kQTileBytes;   // kPSmem: P_t, K-major SW128 [key atom][row][128 B]
+  uint8_t* sExt = smem + NT * C::kQTileBytes + NT * C::kPTileBytes;   // kExt: A_ext(+s), A_ext(-s), B_ext
   uint8_t* sKV = smem + C::kSmemQ;
   float* xchg = reinterpret_cast<float*>(sKV + C::kSmemKV);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::kSmemKV + C::kXchgBytes);
@@ -389,8 +405,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int zb = blockIdx.z;                                 // output batch index (split * B + b)
   const int b = s.kv_splits > 1 ? zb % s.B : zb;              // input batch index
   const int hkv = hq / (s.Hq / s.Hkv);                       // R6: contiguous GQA groups
-  const int row0 = qblk * 2 * BM;
-  Range rng0 = tile_range(s, v, row0), rng1 = tile_range(s, v, row0 + BM);
+  const int row0 = qblk * NT * BM;
+  Range rng0 = tile_range(s, v, row0), rng1 = NT == 2 ? tile_range(s, v, row0 + BM) : Range{0, 0, 0, -1, 0, -1};
   if (s.kv_splits > 1) {   // this CTA's KV split: a contiguous run of whole tiles
     const int t_lo = (zb / s.B) * s.kv_split_tiles, t_hi = t_lo + s.kv_split_tiles;
     for (Range* r : {&rng0, &rng1}) {
@@ -399,7 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (r->lo >= r->hi) r->lo = r->hi = 0;
     }
   }
-  const bool has_rows1 = row0 + BM < s.Sq;
+  const bool has_rows1 = NT == 2 && row0 + BM < s.Sq;
   int ulo = 0, uhi = 0;
   if (rng0.hi > rng0.lo && rng1.hi > rng1.lo) {
     ulo = min(rng0.lo, rng1.lo);
@@ -426,20 +442,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     fence_mbarrier_init();
   }
-  if (warp == kWarpAlloc) tmem_alloc<512>(tmem_slot);
+  if (warp == kWarpAlloc) tmem_alloc<Ro::kTmemCols>(tmem_slot);
   // ALiBi in the contraction (kExt): is it usable for this head?  (fp16 parts must not overflow.)
   bool ext_on = false;
   if constexpr (kExt) {
     const float sx = v.alibi[hq] / v.scale;
     ext_on = kF16 ? fabsf(sx) < 256.f : fabsf(sx) < 1e30f;
-    if (ext_on && threadIdx.x < 2 * BM) {
+    for (int ti = threadIdx.x; ext_on && ti < 2 * BM; ti += blockDim.x) {
       // Row r of A_ext(+-s) = (s_hi, s_mid, s_lo, 0, ...): s split into three 16-bit parts;
       // row c of B_ext = (c, c, c, 0, ...) (c <= 127: exact).  K-major, 128-B swizzle.
-      const int r = threadIdx.x & (BM - 1);
+      const int r = ti & (BM - 1);
       uint4 row[2][8];
       for (int u = 0; u < 2; ++u)
         for (int ch = 0; ch < 8; ++ch) row[u][ch] = make_uint4(0u, 0u, 0u, 0u);
-      if (threadIdx.x < BM) {
+      if (ti < BM) {
         const float hi = round16<kF16>(sx), mid = round16<kF16>(sx - hi), lo = round16<kF16>(sx - hi - mid);
         row[0][0] = make_uint4(pack2<kF16>(hi, mid), pack2<kF16>(lo, 0.f), 0u, 0u);
         row[1][0] = make_uint4(pack2<kF16>(-hi, -mid), pack2<kF16>(-lo, 0.f), 0u, 0u);
@@ -452,8 +468,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int ch = 0; ch < 8; ++ch)
           *reinterpret_cast<uint4*>(sExt + 2 * C::kExtTileBytes + r * 128 + ((ch ^ (r & 7)) << 4)) = row[0][ch];
       }
-      fence_proxy_async_smem();   // generic-proxy stores -> tensor core reads
     }
+    fence_proxy_async_smem();   // generic-proxy stores -> tensor core reads
   }
   tc_fence_before();
   __syncthreads();
@@ -461,8 +477,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) TRACE(3, 0);
 
-  if (warp >= kSoftmaxWarps) {   // warpgroup 2: producer, MMA issuer, TMEM allocator, idle
-  if constexpr (kRegsOther > 0) reg_dealloc<kRegsOther>();
   if (warp == kWarpLoad) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
@@ -540,7 +554,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc_qk = idesc_f16_f32(BM, BN, 0, 0, !kF16);  // Q K-major, K K-major
       constexpr uint32_t idesc_pv = idesc_f16_f32(BM, D, 0, 1, !kF16);   // P (TMEM), V MN-major
       const uint32_t tS[2] = {tmem, tmem + 128};
-      const uint32_t tO[2] = {tmem + 256, tmem + 384};
+      const uint32_t tO[2] = {tmem + Ro::kOBase, tmem + Ro::kOBase + 128};
       const Range rg[2] = {rng0, rng1};
       WAIT_LM(q_full, 0);
 
@@ -666,13 +680,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       }
     }
-  }
-  } else {   // warpgroups 0 and 1: softmax of query tiles 0 and 1
-  if constexpr (kRegsSoftmax > 0) reg_alloc<kRegsSoftmax>();
+  } else if (warp < kSoftmaxWarps) {
     // ------------------------------------------------------------ softmax / correction / epilogue
     // Thread (tile t, row r, column half h) owns S columns [h*kHC, (h+1)*kHC) of row r.
-    const int t = (int)warp / (kSoftmaxWarps / 2);
-    const int wt = (int)warp % (kSoftmaxWarps / 2);       // warp within the tile
+    const int t = (int)warp / (kSoftmaxWarps / NT);
+    const int wt = (int)warp % (kSoftmaxWarps / NT);      // warp within the tile
     const int half = wt >> 2;
     const int wq = warp & 3;                               // TMEM lane quarter
     const int r = wq * 32 + lane;
@@ -687,7 +699,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int kOC = D / kHalves;                       // O columns of this thread
     const uint32_t tS = tmem + t * 128 + lane_off + c_base;
     const uint32_t tP = tmem + t * 128 + lane_off + half * (kHC / 2);   // bf16 pairs, aliasing S
-    const uint32_t tO = tmem + 256 + t * 128 + lane_off + half * kOC;
+    const uint32_t tO = tmem + Ro::kOBase + t * 128 + lane_off + half * kOC;
     float* my_x = xchg + (t * kHalves + half) * BM + r;             // exchange slots (kHalves == 2)
     const float* other_x = xchg + (t * kHalves + (1 - half)) * BM + r;
     const float nslope2 = kAlibi ? -v.alibi[hq] * kLog2e : 0.f;
@@ -939,7 +951,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
   if (warp == kWarpAlloc) {
     tc_fence_after();
-    tmem_dealloc<512>(tmem);
+    tmem_dealloc<Ro::kTmemCols>(tmem);
   }
 }
 
@@ -1068,8 +1080,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp >= kSoftmaxWarps) {   // warpgroup 2: producer, MMA issuer, TMEM allocator, idle
-  if constexpr (kRegsOther > 0) reg_dealloc<kRegsOther>();
   if (warp == kWarpLoad) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
@@ -1197,9 +1207,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int t = 0; t < 2; ++t)      // the softmax's arrival for its last S load
       if (qk_any[t]) named_bar_sync(kBarS0 + t, kTileThreads + 32);
-  }
-  } else {   // warpgroups 0 and 1: softmax of query tiles 0 and 1
-  if constexpr (kRegsSoftmax > 0) reg_alloc<kRegsSoftmax>();
+  } else if (warp < kSoftmaxWarps) {
     // ------------------------------------------------------------ softmax / correction / epilogue
     const int t = (int)warp / 4;
     const int wq = warp & 3;
@@ -1395,16 +1403,17 @@ cudaError_t launch_persist(const FwdTcArgs& a, cudaStream_t stream) {
 
 template <int D, bool kAlibi, bool kSoftcap, bool kF16>
 cudaError_t launch_t(const FwdTcArgs& a, cudaStream_t stream) {
-  using C = Cfg<D, alibi_mma<D, kAlibi && !kSoftcap>()>;
-  if constexpr (D == 128 && C::kPS && kHalves == 1 && !kTraceBuild) {
+  constexpr int NT = D == 128 ? ATTN_NT128 : ATTN_NT64;
+  using C = Cfg<D, alibi_mma<D, kAlibi && !kSoftcap>(), NT>;
+  if constexpr (D == 128 && NT == 2 && C::kPS && kHalves == 1 && !kTraceBuild) {
     const bool pure_causal = a.v.causal && a.v.window_left < 0 && a.v.window_right < 0;
     if (ATTN_PERSIST == 2 || (ATTN_PERSIST == 1 && pure_causal)) return launch_persist<kAlibi, kSoftcap, kF16>(a, stream);
   }
-  auto kern = fwd_tc_kernel<D, kAlibi, kSoftcap, kF16>;
-  cudaError_t e = set_smem_once<fwd_tc_kernel<D, kAlibi, kSoftcap, kF16>>(C::kSmemBytes);
+  auto kern = fwd_tc_kernel<D, kAlibi, kSoftcap, kF16, NT>;
+  cudaError_t e = set_smem_once<fwd_tc_kernel<D, kAlibi, kSoftcap, kF16, NT>>(C::kSmemBytes);
   if (e != cudaSuccess) return e;
-  dim3 grid((a.s.Sq + 2 * BM - 1) / (2 * BM), a.s.Hq, a.s.B * (a.s.kv_splits > 1 ? a.s.kv_splits : 1));
-  kern<<<grid, kThreads, C::kSmemBytes, stream>>>(a.tm_q, a.tm_k, a.tm_v, a.tm_o, a.s, a.v, a.lse);
+  dim3 grid((a.s.Sq + NT * BM - 1) / (NT * BM), a.s.Hq, a.s.B * (a.s.kv_splits > 1 ? a.s.kv_splits : 1));
+  kern<<<grid, Roles<NT>::kThreads, C::kSmemBytes, stream>>>(a.tm_q, a.tm_k, a.tm_v, a.tm_o, a.s, a.v, a.lse);
   return cudaGetLastError();
 }
 

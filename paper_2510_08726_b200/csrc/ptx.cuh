@@ -327,12 +327,6 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   if constexpr (kF16) return pack_f16x2(lo, hi);
   else return pack_bf16x2(lo, hi);
 }
-// Warpgroup register reallocation (all 4 warps of the warpgroup execute it).
-template <int N>
-__device__ __forceinline__ void reg_alloc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N)); }
-template <int N>
-__device__ __forceinline__ void reg_dealloc() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
-
 // x rounded (RNE) to the kernel's 16-bit element type, as a float.
 template <bool kF16>
 __device__ __forceinline__ float round16(float x) {
