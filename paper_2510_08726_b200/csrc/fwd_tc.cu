@@ -168,12 +168,12 @@ struct Cfg {
 #ifndef ATTN_P_SMEM64
 #define ATTN_P_SMEM64 0
 #endif
-  static constexpr bool kPS = NT == 1 ? false : (D == 128 ? kPSmem : ATTN_P_SMEM64 != 0);
+  static constexpr bool kPS = NT == 1 ? (D == 64 && !kExt && ATTN_P_SMEM64 != 0) : (D == 128 ? kPSmem : ATTN_P_SMEM64 != 0);
   static constexpr int kPTileBytes = kPS ? BM * BN * 2 : 0;
 #ifdef ATTN_TRACE
   static constexpr int kStages = kPS ? 3 : ((D == 128) ? 4 : 8);   // room for the trace
 #else
-  static constexpr int kStages = NT == 1 ? ((D == 128) ? 2 : (kExt ? 3 : ATTN_NT1_STAGES64))
+  static constexpr int kStages = NT == 1 ? ((D == 128) ? 2 : (kExt ? 3 : (kPS ? 4 : ATTN_NT1_STAGES64)))
                                           : kPS ? ((D == 128) ? 3 : 6) : ((D == 128) ? 5 : (kExt ? 8 : ATTN_D64_STAGES));
 #endif
   // Load-group barriers (ring).  The producer can be at most kStages/2 groups
@@ -243,6 +243,9 @@ __device__ __forceinline__ float ex2_poly(float x) {
 
 #ifndef ATTN_POLY_DIV
 #define ATTN_POLY_DIV 0   // every ATTN_POLY_DIV-th pair of exponentials uses ex2_poly (0 = none)
+#endif
+#ifndef ATTN_POLY_DIV64
+#define ATTN_POLY_DIV64 0
 #endif
 
 __device__ __forceinline__ bool active(const Range& r, int j) { return j >= r.lo && j < r.hi; }
@@ -374,6 +377,7 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
   constexpr bool kPSmem = C::kPS;   // shadows the global switch: per head dim
   constexpr bool kF32x2 = D == 128 ? ::attn::kF32x2 : ATTN_F32X2_64 != 0;   // measured: +1.5-2 % at D = 128, -4 % at D = 64
   constexpr bool kToken = NT == 2 && (D == 128 ? ::attn::kToken : ATTN_TOKEN64 != 0);
+  constexpr int kPolyDiv = D == 64 ? ATTN_POLY_DIV64 : ATTN_POLY_DIV;   // pairs on the FMA-pipe exp2
   constexpr bool kPlain = !kAlibi && !kSoftcap;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // The 128-byte swizzle needs 1024-byte aligned tiles; dynamic shared memory
@@ -820,7 +824,7 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
             a1 = x[c0 + 2 * e + 1] - m_use_t;
           }
           float p0, p1;
-          if (ATTN_POLY_DIV > 0 && (e % (ATTN_POLY_DIV > 0 ? ATTN_POLY_DIV : 1)) == (ATTN_POLY_DIV > 0 ? ATTN_POLY_DIV : 1) - 1) {
+          if (kPolyDiv > 0 && (e % (kPolyDiv > 0 ? kPolyDiv : 1)) == (kPolyDiv > 0 ? kPolyDiv : 1) - 1) {
             p0 = ex2_poly(a0);
             p1 = ex2_poly(a1);
           } else {
