@@ -79,7 +79,7 @@ def load_peaks():
 
 
 class ClockSampler:
-    """SM clock and clock-event (throttle) reasons sampled every 10 ms during the
+    """SM clock and clock-event (throttle) reasons sampled every 2 ms during the
     timed region, through NVML (nvidia-smi's library)."""
 
     REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
@@ -115,7 +115,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception as e:  # noqa: BLE001
                 self.err = str(e)
-            self._stop.wait(0.01)
+            self._stop.wait(0.002)
 
     def __exit__(self, *a):
         self._stop.set()
