@@ -92,6 +92,9 @@ constexpr bool kToken = ATTN_TOKEN != 0;   // alternate the two softmax warpgrou
 #ifndef ATTN_TOKEN64
 #define ATTN_TOKEN64 ATTN_TOKEN
 #endif
+#ifndef ATTN_TOKEN_RELEASE
+#define ATTN_TOKEN_RELEASE 4
+#endif
 #ifndef ATTN_F32X2_64
 #define ATTN_F32X2_64 0
 #endif
@@ -378,6 +381,9 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
   constexpr bool kF32x2 = D == 128 ? ::attn::kF32x2 : ATTN_F32X2_64 != 0;   // measured: +1.5-2 % at D = 128, -4 % at D = 64
   constexpr bool kToken = NT == 2 && (D == 128 ? ::attn::kToken : ATTN_TOKEN64 != 0);
   constexpr int kPolyDiv = D == 64 ? ATTN_POLY_DIV64 : ATTN_POLY_DIV;   // pairs on the FMA-pipe exp2
+  // The token passes to the other tile after this many of the row's 32-column exp chunks
+  // (4 = after the whole exp phase): an earlier release overlaps the two tiles' exp phases.
+  constexpr int kTokenRelease = ATTN_TOKEN_RELEASE;
   constexpr bool kPlain = !kAlibi && !kSoftcap;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // The 128-byte swizzle needs 1024-byte aligned tiles; dynamic shared memory
@@ -851,11 +857,15 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
         } else {
           tmem_st16(tP + c0 / 2, pk);
         }
+        if (kToken && kTokenRelease < kHC / 32 && c0 == (kTokenRelease - 1) * 32) {   // early token release
+          if (t == 0) named_bar_arrive(kBarTok1, 2 * kTileThreads);
+          else if (j + 1 < uhi) named_bar_arrive(kBarTok0, 2 * kTileThreads);
+        }
       }
 #ifdef ATTN_TOKEN_STRICT
       if (kToken) asm volatile("" ::"f"(sum0), "f"(sum1));
 #endif
-      if (kToken) {                                         // release the token
+      if (kToken && kTokenRelease >= kHC / 32) {            // release the token
         if (t == 0) named_bar_arrive(kBarTok1, 2 * kTileThreads);
         else if (j + 1 < uhi) named_bar_arrive(kBarTok0, 2 * kTileThreads);
       }
