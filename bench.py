@@ -48,6 +48,9 @@ WORKLOADS = {
     "var_causal": (4, 8, 16, 16, 2048, 64, dict(causal=True)),
     "var_alibi": (4, 8, 16, 16, 2048, 64, dict(alibi=True)),
     "var_softcap": (4, 8, 16, 16, 2048, 64, dict(softcap=50.0)),
+    # ALiBi at D = 128 on the config-2 shape (the paper's MPT-7B ALiBi operator has D = 128)
+    "mha_alibi": (2, 8, 16, 16, 4096, 128, dict(alibi=True)),
+    "mha_alibi_causal": (2, 8, 16, 16, 4096, 128, dict(causal=True, alibi=True)),
 }
 
 

@@ -135,6 +135,12 @@ __device__ __forceinline__ bool trace_cta() { return blockIdx.x == 5 && blockIdx
 #ifndef ATTN_ALIBI_MMA
 #define ATTN_ALIBI_MMA 1
 #endif
+#ifndef ATTN_ALIBI_REV
+#define ATTN_ALIBI_REV 1
+#endif
+#ifndef ATTN_ALIBI_CAUSAL_LIN
+#define ATTN_ALIBI_CAUSAL_LIN 1
+#endif
 // ALiBi folded into the QK contraction (D = 64, where the tensor core has slack): one
 // extra K = 16 MMA step adds s*c (s = slope / scale split into three 16-bit parts, c = key
 // column in the tile) to S, so the per-element bias costs nothing on the FMA pipe (see
@@ -258,6 +264,9 @@ __device__ __forceinline__ bool active(const Range& r, int j) { return j >= r.lo
 // A_ext(+s)), -1 if every key is at or after every query (A_ext(-s)), 0 mixed (A_ext(+s) and
 // a per-element fix-up).  The issuer and the softmax threads classify identically.
 __device__ __forceinline__ int ext_class(const Shape& s, const VariantParams& v, int i0, int j) {
+  // Causal: every ALLOWED key of any tile is at or before its query, so the linear form holds
+  // for the allowed elements of a diagonal tile too (the rest are masked to -inf).
+  if (v.causal && ATTN_ALIBI_CAUSAL_LIN) return 1;
   const long long qf = v.q_off + i0, ql = v.q_off + min(i0 + BM, s.Sq) - 1;
   const long long k0 = v.kv_off + (long long)j * BN, k1 = k0 + BN - 1;
   if (k1 <= qf) return 1;
@@ -344,6 +353,22 @@ __device__ __forceinline__ float score_tile(float (&x)[N], const VariantParams& 
   return mt;
 }
 
+#ifndef ATTN_ALIBI_LIN
+#define ATTN_ALIBI_LIN 1
+#endif
+
+// ALiBi on a tile of uniform sign (ext_class != 0) without the MMA extension: the bias is
+// sslope * c + a row constant (folded into the exponent's offset by the caller), so
+// x = scale S + sslope * c costs an immediate-operand multiply and one FFMA per element
+// instead of FMUL + |.| FADD + FFMA (the FMA pipe bound the ALiBi kernels at D = 128).
+template <bool kMask, bool kChunked, int N>
+__device__ __forceinline__ float score_tile_alibi_lin(float (&x)[N], const VariantParams& v, float sslope, int rel_lo,
+                                                      int rel_hi) {
+  return row_max_pass<kMask, kChunked>(x, rel_lo, rel_hi, [&](float xv, int c) {
+    return fmaf(xv, v.scale_log2, sslope * (float)c);
+  });
+}
+
 // Mixed ALiBi-in-MMA tile (ext_class 0, built with A_ext(+s)): S = q.k + s c, so
 // x = scale S - slope (c + |qpos - kpos|) = scale S - slope max(dq0, 2c - dq0) (log2 units).
 template <bool kMask, int N>
@@ -372,6 +397,7 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o, const Shape s,
                   const VariantParams v, float* __restrict__ lse) {
   constexpr bool kExt = alibi_mma<D, kAlibi && !kSoftcap>();   // softcap: the bias follows the tanh
+  constexpr bool kAlibiLin = ATTN_ALIBI_LIN != 0 && kAlibi && !kSoftcap && !kExt;   // uniform-tile ALiBi, FMA form
   constexpr bool kChunkMask = D == 128 && ATTN_CHUNK_MASK;   // chunk-classified masking (measured: + at D = 128, - at D = 64)
   using C = Cfg<D, kExt, NT>;
   using Ro = Roles<NT>;
@@ -435,6 +461,20 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
   } else if (rng1.hi > rng1.lo) {
     ulo = rng1.lo; uhi = rng1.hi;
   }
+  // KV order.  Rolling Update is exact in any order (Thm. 3-4); with ALiBi and keys only at or
+  // before the queries the bias grows toward the diagonal, so the ascending order raises the
+  // running max by slope * 128 per tile and repairs O every step.  Those problems walk the KV
+  // tiles from the diagonal down (the first tile holds the max): step k visits tile J(k).  The
+  // loops below count steps k in [ulo, uhi); rng0/rng1 lo/hi are mapped to step space.
+  const bool rev = kAlibi && ATTN_ALIBI_REV && (v.causal || v.window_right == 0);
+  auto J = [=](int k) { return rev ? ulo + uhi - 1 - k : k; };
+  if (rev)
+    for (Range* r : {&rng0, &rng1})
+      if (r->hi > r->lo) {
+        const int lo = ulo + uhi - r->hi, hi = ulo + uhi - r->lo;
+        r->lo = lo;
+        r->hi = hi;
+      }
 
   if (warp == kWarpLoad && lane == 0) {
     prefetch_tmap(&tm_q);
@@ -504,8 +544,8 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
       if (kPrefetch > 0)
       for (int j = ulo; j < min(ulo + kPrefetch, uhi); ++j)
         for (int bx = 0; bx < C::kBoxes; ++bx) {
-          tma_prefetch_4d(&tm_k, bx * 64, j * BN, hkv, b);
-          tma_prefetch_4d(&tm_v, bx * 64, j * BN, hkv, b);
+          tma_prefetch_4d(&tm_k, bx * 64, J(j) * BN, hkv, b);
+          tma_prefetch_4d(&tm_v, bx * 64, J(j) * BN, hkv, b);
         }
       if constexpr (kPSmem) {
         // One barrier per ring slot; ring order = the issuer's consumption order:
@@ -517,7 +557,7 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
           mbar_arrive_expect_tx(bar, C::kKVTileBytes);
           uint8_t* dst = sKV + (it % C::kStages) * C::kKVTileBytes;
           for (int bx = 0; bx < C::kBoxes; ++bx)
-            tma_load_4d(is_k ? &tm_k : &tm_v, bar, dst + bx * BN * 128, bx * 64, jj * BN, hkv, b, pol_kv);
+            tma_load_4d(is_k ? &tm_k : &tm_v, bar, dst + bx * BN * 128, bx * 64, J(jj) * BN, hkv, b, pol_kv);
           ++it;
         };
         if (uhi > ulo) {
@@ -537,8 +577,8 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
         const int j = ulo + g;
         if (kPrefetch > 0 && j + kPrefetch < uhi)
           for (int bx = 0; bx < C::kBoxes; ++bx) {
-            tma_prefetch_4d(&tm_k, bx * 64, (j + kPrefetch) * BN, hkv, b);
-            tma_prefetch_4d(&tm_v, bx * 64, (j + kPrefetch) * BN, hkv, b);
+            tma_prefetch_4d(&tm_k, bx * 64, J(j + kPrefetch) * BN, hkv, b);
+            tma_prefetch_4d(&tm_v, bx * 64, J(j + kPrefetch) * BN, hkv, b);
           }
         const int it0 = g == 0 ? 0 : 2 * g - 1;          // ring index of the group's first tile
         const int it1 = g < n ? 2 * g : 2 * g - 1;       // ... and of its last tile
@@ -551,7 +591,7 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
           TRACE(24 + (is_k ? 0 : 1), jj);
           uint8_t* dst = sKV + (it % C::kStages) * C::kKVTileBytes;
           for (int bx = 0; bx < C::kBoxes; ++bx)
-            tma_load_4d(is_k ? &tm_k : &tm_v, bar, dst + bx * BN * 128, bx * 64, jj * BN, hkv, b, pol_kv);
+            tma_load_4d(is_k ? &tm_k : &tm_v, bar, dst + bx * BN * 128, bx * 64, J(jj) * BN, hkv, b, pol_kv);
         }
       }
       }
@@ -584,7 +624,7 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
         }
         if constexpr (kExt) {
           if (ext_on && !ATTN_EXT_NOMMA) {
-            const int cls = ext_class(s, v, row0 + t * BM, j);
+            const int cls = ext_class(s, v, row0 + t * BM, J(j));
             const uint32_t sa = smem_u32(sExt + (cls < 0 ? C::kExtTileBytes : 0));
             mma_ss_warp(tS[t], smem_desc_sw128(sa, 16, 1024), smem_desc_sw128(smem_u32(sExt + 2 * C::kExtTileBytes), 16, 1024),
                         idesc_qk, 1u);
@@ -748,15 +788,16 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
         for (int c = 0; c < kHC; ++c) x[c] = u2f(u[c]);
       }
       // Fig. 19 max_local (+ score_mod, mask) -> max_global
-      const bool need_mask = !(j * BN >= R.jlo_last && (j + 1) * BN - 1 <= R.jhi_first);
-      const int rel_lo = jlo_row - j * BN - c_base, rel_hi = jhi_row - j * BN - c_base;
-      const float dq0 = (float)(qpos - v.kv_off - (long long)j * BN - c_base);
+      const int jt = J(j);   // the KV tile of step j
+      const bool need_mask = !(jt * BN >= R.jlo_last && (jt + 1) * BN - 1 <= R.jhi_first);
+      const int rel_lo = jlo_row - jt * BN - c_base, rel_hi = jhi_row - jt * BN - c_base;
+      const float dq0 = (float)(qpos - v.kv_off - (long long)jt * BN - c_base);
       // exponent argument a = x * e_mul + e_off' (e_off' = e_off - m, set after the max)
       float e_mul = kPlain ? v.scale_log2 : 1.f, e_off = 0.f;
       float mt;
       if (kExt && ext_on) {
         // ALiBi in the contraction: S already holds q.k + (+-s) c (see ext_class)
-        const int cls = ext_class(s, v, row0 + t * BM, j);
+        const int cls = ext_class(s, v, row0 + t * BM, jt);
         if (cls != 0) {   // bias = row constant: the plain path with an offset
           e_mul = v.scale_log2;
           e_off = (cls > 0 ? nslope2 : -nslope2) * dq0;
@@ -766,6 +807,12 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
           mt = need_mask ? score_tile_ext_mixed<true>(x, v, nslope2, dq0, rel_lo, rel_hi)
                          : score_tile_ext_mixed<false>(x, v, nslope2, dq0, rel_lo, rel_hi);
         }
+      } else if (kAlibiLin && ext_class(s, v, row0 + t * BM, jt) != 0) {
+        const int cls = ext_class(s, v, row0 + t * BM, jt);
+        e_off = (cls > 0 ? nslope2 : -nslope2) * dq0;
+        const float sslope = cls > 0 ? -nslope2 : nslope2;
+        mt = (need_mask ? score_tile_alibi_lin<true, kChunkMask>(x, v, sslope, rel_lo, rel_hi)
+                        : score_tile_alibi_lin<false, kChunkMask>(x, v, sslope, rel_lo, rel_hi)) + e_off;
       } else {
         mt = need_mask ? score_tile<kAlibi, kSoftcap, true, kChunkMask>(x, v, nslope2, dq0, rel_lo, rel_hi)
                        : score_tile<kAlibi, kSoftcap, false, kChunkMask>(x, v, nslope2, dq0, rel_lo, rel_hi);
@@ -815,11 +862,11 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           float a0, a1;
-          if constexpr (kF32x2 && kExt) {
+          if constexpr (kF32x2 && (kExt || kAlibiLin)) {
             fma2_bc(a0, a1, x[c0 + 2 * e], x[c0 + 2 * e + 1], e_mul, e_add);
           } else if constexpr (kF32x2) {
             fma2_bc(a0, a1, x[c0 + 2 * e], x[c0 + 2 * e + 1], kPlain ? v.scale_log2 : 1.f, -m_use_t);
-          } else if constexpr (kExt) {
+          } else if constexpr (kExt || kAlibiLin) {
             a0 = fmaf(x[c0 + 2 * e], e_mul, e_add);
             a1 = fmaf(x[c0 + 2 * e + 1], e_mul, e_add);
           } else if constexpr (kPlain) {
@@ -1263,8 +1310,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool need_mask = !(j * BN >= R.jlo_last && (j + 1) * BN - 1 <= R.jhi_first);
         const int rel_lo = jlo_row - j * BN, rel_hi = jhi_row - j * BN;
         const float dq0 = (float)(qpos - v.kv_off - (long long)j * BN);
-        const float mt = need_mask ? score_tile<kAlibi, kSoftcap, true, ATTN_CHUNK_MASK != 0>(x, v, nslope2, dq0, rel_lo, rel_hi)
-                                   : score_tile<kAlibi, kSoftcap, false, ATTN_CHUNK_MASK != 0>(x, v, nslope2, dq0, rel_lo, rel_hi);
+        constexpr bool kAlibiLin = ATTN_ALIBI_LIN != 0 && kAlibi && !kSoftcap;
+        constexpr bool kCh = ATTN_CHUNK_MASK != 0;
+        float mt, e_off = 0.f;
+        if (kAlibiLin && ext_class(s, v, row0 + t * BM, j) != 0) {   // see score_tile_alibi_lin
+          const int cls = ext_class(s, v, row0 + t * BM, j);
+          e_off = (cls > 0 ? nslope2 : -nslope2) * dq0;
+          const float sslope = cls > 0 ? -nslope2 : nslope2;
+          mt = (need_mask ? score_tile_alibi_lin<true, kCh>(x, v, sslope, rel_lo, rel_hi)
+                          : score_tile_alibi_lin<false, kCh>(x, v, sslope, rel_lo, rel_hi)) + e_off;
+        } else {
+          mt = need_mask ? score_tile<kAlibi, kSoftcap, true, kCh>(x, v, nslope2, dq0, rel_lo, rel_hi)
+                         : score_tile<kAlibi, kSoftcap, false, kCh>(x, v, nslope2, dq0, rel_lo, rel_hi);
+        }
         const float m_run = fmaxf(m_ref, mt);
         bool move, need_o;
         if (m_ref == -INFINITY) {
@@ -1279,6 +1337,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (move) m_ref = m_run;
         l *= alpha;
         const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
+        const float e_add = e_off - m_use;   // (e_off: the ALiBi row constant of a uniform tile, else 0)
         if (n_pv > 0) {                 // PV_t of the previous step (maybe of the previous unit) is done
           mbar_wait(&o_done[t], (n_pv - 1) & 1);
           tc_fence_after();
@@ -1291,13 +1350,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int e = 0; e < 16; ++e) {
             float a0, a1;
             if constexpr (kF32x2) {
-              fma2_bc(a0, a1, x[c0 + 2 * e], x[c0 + 2 * e + 1], kPlain ? v.scale_log2 : 1.f, -m_use);
+              fma2_bc(a0, a1, x[c0 + 2 * e], x[c0 + 2 * e + 1], kPlain ? v.scale_log2 : 1.f, e_add);
             } else if constexpr (kPlain) {
-              a0 = fmaf(x[c0 + 2 * e], v.scale_log2, -m_use);
-              a1 = fmaf(x[c0 + 2 * e + 1], v.scale_log2, -m_use);
+              a0 = fmaf(x[c0 + 2 * e], v.scale_log2, e_add);
+              a1 = fmaf(x[c0 + 2 * e + 1], v.scale_log2, e_add);
             } else {
-              a0 = x[c0 + 2 * e] - m_use;
-              a1 = x[c0 + 2 * e + 1] - m_use;
+              a0 = x[c0 + 2 * e] + e_add;
+              a1 = x[c0 + 2 * e + 1] + e_add;
             }
             const float p0 = ex2_approx(a0), p1 = ex2_approx(a1);
             if constexpr (kF32x2) {
@@ -1421,7 +1480,8 @@ cudaError_t launch_t(const FwdTcArgs& a, cudaStream_t stream) {
   using C = Cfg<D, alibi_mma<D, kAlibi && !kSoftcap>(), NT>;
   if constexpr (D == 128 && NT == 2 && C::kPS && kHalves == 1 && !kTraceBuild) {
     const bool pure_causal = a.v.causal && a.v.window_left < 0 && a.v.window_right < 0;
-    if (ATTN_PERSIST == 2 || (ATTN_PERSIST == 1 && pure_causal)) return launch_persist<kAlibi, kSoftcap, kF16>(a, stream);
+    // (ALiBi stays on the grid kernel: it walks the KV tiles diagonal-first, see J in fwd_tc_kernel)
+    if (ATTN_PERSIST == 2 || (ATTN_PERSIST == 1 && pure_causal && !kAlibi)) return launch_persist<kAlibi, kSoftcap, kF16>(a, stream);
   }
   auto kern = fwd_tc_kernel<D, kAlibi, kSoftcap, kF16, NT>;
   cudaError_t e = set_smem_once<fwd_tc_kernel<D, kAlibi, kSoftcap, kF16, NT>>(C::kSmemBytes);

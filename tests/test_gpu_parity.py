@@ -134,9 +134,11 @@ def test_bf16_prefill_rectangular(Sq, Skv, extra):
     (200, 600, dict(scale=1e-3)),                                          # |slope / scale| = 707: large ALiBi term
 ])
 @pytest.mark.parametrize("dtype", ["bf16", "fp16"])
-def test_alibi_d64_rectangular(Sq, Skv, extra, dtype):
-    """ALiBi at D = 64 (bias folded into the QK contraction; fp16 with |s| >= 256 falls back)."""
-    _rectangular(Sq, Skv, dict(extra, alibi_slopes=datagen.alibi_slopes(4)), 64, Hq=4, Hkv=2, dtype=dtype)
+@pytest.mark.parametrize("D", [64, 128])
+def test_alibi_rectangular(Sq, Skv, extra, dtype, D):
+    """ALiBi by tile class: D = 64 folds the bias into the QK contraction (fp16 with |s| >= 256
+    falls back); D = 128 uses the linear form on tiles of uniform sign; both fix up mixed tiles."""
+    _rectangular(Sq, Skv, dict(extra, alibi_slopes=datagen.alibi_slopes(4)), D, Hq=4, Hkv=2, dtype=dtype)
 
 
 def _rectangular(Sq, Skv, extra, D, Hq=2, Hkv=1, dtype="bf16"):
@@ -229,6 +231,7 @@ FULL = {
     "variants_scaled_dot": dict(cid=4, B=8, Hq=16, Hkv=16, S=2048, D=64),
     "variants_alibi_causal": dict(cid=4, B=8, Hq=16, Hkv=16, S=2048, D=64, causal=True, alibi=True),
     "variants_alibi": dict(cid=4, B=8, Hq=16, Hkv=16, S=2048, D=64, alibi=True),
+    "mha_alibi_causal": dict(cid=2, B=8, Hq=16, Hkv=16, S=4096, D=128, causal=True, alibi=True),
     "variants_softcap_causal": dict(cid=4, B=8, Hq=16, Hkv=16, S=2048, D=64, causal=True, softcap=2.0),
 }
 
