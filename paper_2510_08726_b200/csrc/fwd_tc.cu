@@ -466,8 +466,22 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
   // running max by slope * 128 per tile and repairs O every step.  Those problems walk the KV
   // tiles from the diagonal down (the first tile holds the max): step k visits tile J(k).  The
   // loops below count steps k in [ulo, uhi); rng0/rng1 lo/hi are mapped to step space.
+  // Without a mask edge inside [ulo, uhi) (both tiles span it) the walk starts at the CTA's
+  // diagonal tile d, goes down to ulo, then up from d + 1: J(k) = d - (k - ulo) for the first
+  // d - ulo + 1 steps, else k (the reflection above is the case d = uhi - 1).
+  const bool full = (rng0.lo == ulo && rng0.hi == uhi) && (!has_rows1 || (rng1.lo == ulo && rng1.hi == uhi));
   const bool rev = kAlibi && ATTN_ALIBI_REV && (v.causal || v.window_right == 0);
-  auto J = [=](int k) { return rev ? ulo + uhi - 1 - k : k; };
+  int d_walk = ulo - 1;   // identity
+  if (rev) {
+    d_walk = uhi - 1;
+  } else if (kAlibi && ATTN_ALIBI_REV && full && uhi > ulo) {
+    const long long ql = v.q_off + min(row0 + NT * BM, s.Sq) - 1;
+    d_walk = (int)max((long long)ulo, min((long long)uhi - 1, (ql - v.kv_off) / BN));
+  }
+  auto J = [=](int k) {
+    if constexpr (kAlibi) return k - ulo <= d_walk - ulo ? d_walk - (k - ulo) : k;
+    else return k;
+  };
   if (rev)
     for (Range* r : {&rng0, &rng1})
       if (r->hi > r->lo) {
