@@ -5,7 +5,7 @@ TAG=${1:-ck}
 timeout 1200 python -m pytest tests -m gpu -q --timeout 300 -p no:cacheprovider > gpurun_out/pytest_$TAG.log 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1
 timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
-for w in mha_causal gqa_window var_scaled_dot var_alibi_causal var_softcap_causal; do
+for w in mha_causal gqa_window var_scaled_dot var_alibi_causal var_softcap_causal var_causal var_alibi mha_alibi mha_alibi_causal; do
   timeout 300 python bench.py --steps 20 --warmup 5 --no-e2e --no-decode --no-cpu --no-softmax --workload $w >> gpurun_out/bench_workloads_$TAG.jsonl 2>/dev/null
 done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv \
