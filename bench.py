@@ -82,7 +82,7 @@ def load_peaks():
 
 
 class ClockSampler:
-    """SM clock and clock-event (throttle) reasons sampled every 2 ms during the
+    """SM clock (every ~1 ms) and clock-event (throttle) reasons sampled during the
     timed region, through NVML (nvidia-smi's library)."""
 
     REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
@@ -109,16 +109,19 @@ class ClockSampler:
     def _run(self):
         nv = self.nv
         get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        i = 0
         while not self._stop.is_set():
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-                r = get_r(self.h)
-                for bit, name in self.REASONS.items():
-                    if r & bit:
-                        self.reasons.add(name)
+                if i % 4 == 0:   # the reasons query is the slow one
+                    r = get_r(self.h)
+                    for bit, name in self.REASONS.items():
+                        if r & bit:
+                            self.reasons.add(name)
             except Exception as e:  # noqa: BLE001
                 self.err = str(e)
-            self._stop.wait(0.002)
+            i += 1
+            self._stop.wait(0.001)
 
     def __exit__(self, *a):
         self._stop.set()
