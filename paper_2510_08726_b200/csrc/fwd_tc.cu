@@ -293,6 +293,9 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
 #ifndef ATTN_CHUNK_MASK
 #define ATTN_CHUNK_MASK 1
 #endif
+#ifndef ATTN_CHUNK_MASK64
+#define ATTN_CHUNK_MASK64 0
+#endif
 // (kChunked = false: every element of a mask tile is compared; measured better at D = 64,
 // where the chunk branches cost registers in the MUFU-bound kernels.)
 template <bool kMask, bool kChunked, int N, class XF>
@@ -398,7 +401,7 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
                   const VariantParams v, float* __restrict__ lse) {
   constexpr bool kExt = alibi_mma<D, kAlibi && !kSoftcap>();   // softcap: the bias follows the tanh
   constexpr bool kAlibiLin = ATTN_ALIBI_LIN != 0 && kAlibi && !kSoftcap && !kExt;   // uniform-tile ALiBi, FMA form
-  constexpr bool kChunkMask = D == 128 && ATTN_CHUNK_MASK;   // chunk-classified masking (measured: + at D = 128, - at D = 64)
+  constexpr bool kChunkMask = (D == 128 || ATTN_CHUNK_MASK64) && ATTN_CHUNK_MASK;   // chunk-classified masking (measured: + at D = 128, - at D = 64)
   using C = Cfg<D, kExt, NT>;
   using Ro = Roles<NT>;
   constexpr int kSoftmaxWarps = Ro::kSoftmaxWarps, kWarpLoad = Ro::kWarpLoad, kWarpMma = Ro::kWarpMma;
