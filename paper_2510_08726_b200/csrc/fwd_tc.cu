@@ -145,9 +145,6 @@ __device__ __forceinline__ bool trace_cta() { return blockIdx.x == 5 && blockIdx
 // extra K = 16 MMA step adds s*c (s = slope / scale split into three 16-bit parts, c = key
 // column in the tile) to S, so the per-element bias costs nothing on the FMA pipe (see
 // score_tile_alibi_mma).  Shared memory for the constant operands: A_ext(+s), A_ext(-s), B_ext.
-#ifndef ATTN_EXT_NOMMA
-#define ATTN_EXT_NOMMA 0   // timing experiment only: skip the extra MMA (wrong results)
-#endif
 template <int D, bool kAlibi>
 __host__ __device__ constexpr bool alibi_mma() { return ATTN_ALIBI_MMA != 0 && kAlibi && D == 64; }
 
@@ -640,7 +637,7 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
                  kk > 0 ? 1u : 0u);
         }
         if constexpr (kExt) {
-          if (ext_on && !ATTN_EXT_NOMMA) {
+          if (ext_on) {
             const int cls = ext_class(s, v, row0 + t * BM, J(j));
             const uint32_t sa = smem_u32(sExt + (cls < 0 ? C::kExtTileBytes : 0));
             mma_ss_warp(tS[t], smem_desc_sw128(sa, 16, 1024), smem_desc_sw128(smem_u32(sExt + 2 * C::kExtTileBytes), 16, 1024),
