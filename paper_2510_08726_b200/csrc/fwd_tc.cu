@@ -132,8 +132,20 @@ __device__ __forceinline__ bool trace_cta() { return blockIdx.x == 5 && blockIdx
 #define TRACE(ev, step) do { } while (0)
 #endif
 
+#ifndef ATTN_NT64
+#define ATTN_NT64 1   // measured (same box): causal D = 64 +5 %, scaled-dot +1 %
+#endif
+#ifndef ATTN_NT1_STAGES64
+#define ATTN_NT1_STAGES64 5
+#endif
+#ifndef ATTN_NT128
+#define ATTN_NT128 2   // NT = 1 at D = 128 (TMEM-aliased P, 2-slot ring): -11 % (MHA)
+#endif
 #ifndef ATTN_ALIBI_MMA
 #define ATTN_ALIBI_MMA 1
+#endif
+#ifndef ATTN_ALIBI_MMA128
+#define ATTN_ALIBI_MMA128 1
 #endif
 #ifndef ATTN_ALIBI_REV
 #define ATTN_ALIBI_REV 1
@@ -146,19 +158,12 @@ __device__ __forceinline__ bool trace_cta() { return blockIdx.x == 5 && blockIdx
 // column in the tile) to S, so the per-element bias costs nothing on the FMA pipe (see
 // score_tile_alibi_mma).  Shared memory for the constant operands: A_ext(+s), A_ext(-s), B_ext.
 template <int D, bool kAlibi>
-__host__ __device__ constexpr bool alibi_mma() { return ATTN_ALIBI_MMA != 0 && kAlibi && D == 64; }
+__host__ __device__ constexpr bool alibi_mma() {
+  return ATTN_ALIBI_MMA != 0 && kAlibi && (D == 64 || (D == 128 && ATTN_ALIBI_MMA128 != 0 && ATTN_NT128 == 2 && kPSmem));
+}
 
 #ifndef ATTN_D64_STAGES
 #define ATTN_D64_STAGES 10
-#endif
-#ifndef ATTN_NT64
-#define ATTN_NT64 1   // measured (same box): causal D = 64 +5 %, scaled-dot +1 %
-#endif
-#ifndef ATTN_NT1_STAGES64
-#define ATTN_NT1_STAGES64 5
-#endif
-#ifndef ATTN_NT128
-#define ATTN_NT128 2   // NT = 1 at D = 128 (TMEM-aliased P, 2-slot ring): -11 % (MHA)
 #endif
 // NT = query tiles per CTA.  NT = 2: one CTA per SM, its two tiles' exp phases alternate
 // (token).  NT = 1: 128-row CTAs, TWO resident per SM (256 TMEM columns and < 113 KiB of
@@ -186,15 +191,19 @@ struct Cfg {
   // ahead of the issuer's wait, so kStages/2 + 1 barriers never alias a phase.
   static constexpr int kPairBars = kStages / 2 + 1;
   static constexpr int kExtTileBytes = BM * 128;                     // one 128-B swizzle atom wide
-  static constexpr int kExtBytes = kExt ? 3 * kExtTileBytes : 0;     // A_ext(+s), A_ext(-s), B_ext
+  static constexpr int kExtBytes = (kExt && D == 64) ? 3 * kExtTileBytes : 0;     // A_ext(+s), A_ext(-s), B_ext
+  // D = 128: the tiles above leave only 3 KB, so the operands go after the K/V ring without
+  // swizzle: A_ext(+-s) 2 x 256 B (two K core matrices, all 128 rows aliased by SBO = 0) and
+  // B_ext 2 KB (16 row groups; its K 8..15 half aliases K 0..7 by LBO = 0 and meets zeros in A).
+  static constexpr int kExt2Bytes = (kExt && D == 128) ? 2 * 256 + 2048 : 0;
   static constexpr int kSmemQ = NT * kQTileBytes + NT * kPTileBytes + kExtBytes;   // Q, P, ext tiles
   static constexpr int kSmemKV = kStages * kKVTileBytes;
   static constexpr int kNumBars = 1 + 2 * kStages + 6;
   static constexpr int kXchgBytes = kHalves > 1 ? 2 * kHalves * BM * 4 : 0;   // [tile][half][row] floats
 #ifdef ATTN_TRACE
-  static constexpr int kSmemBytes = kSmemQ + kSmemKV + kXchgBytes + 256 + kTrEv * kTrSteps * 4;
+  static constexpr int kSmemBytes = kSmemQ + kSmemKV + kExt2Bytes + kXchgBytes + 256 + kTrEv * kTrSteps * 4;
 #else
-  static constexpr int kSmemBytes = kSmemQ + kSmemKV + kXchgBytes + kNumBars * 8 + 16;
+  static constexpr int kSmemBytes = kSmemQ + kSmemKV + kExt2Bytes + kXchgBytes + kNumBars * 8 + 16;
 #endif
 };
 
@@ -418,10 +427,11 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
   uint8_t* smem = smem_raw;
   uint8_t* sQ = smem;
   uint8_t* sP = smem + NT * C::kQTileBytes;   // kPSmem: P_t, K-major SW128 [key atom][row][128 B]
-  uint8_t* sExt = smem + NT * C::kQTileBytes + NT * C::kPTileBytes;   // kExt: A_ext(+s), A_ext(-s), B_ext
+  // kExt: A_ext(+s), A_ext(-s), B_ext (D = 64: swizzled tiles after Q; D = 128: after the ring)
+  uint8_t* sExt = D == 64 ? smem + NT * C::kQTileBytes + NT * C::kPTileBytes : smem + C::kSmemQ + C::kSmemKV;
   uint8_t* sKV = smem + C::kSmemQ;
-  float* xchg = reinterpret_cast<float*>(sKV + C::kSmemKV);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::kSmemKV + C::kXchgBytes);
+  float* xchg = reinterpret_cast<float*>(sKV + C::kSmemKV + C::kExt2Bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::kSmemKV + C::kExt2Bytes + C::kXchgBytes);
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;
   uint64_t* kv_empty = kv_full + C::kStages;
@@ -430,7 +440,7 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
   uint64_t* o_done = p_ready + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 #ifdef ATTN_TRACE
-  uint32_t* s_trace = reinterpret_cast<uint32_t*>(smem + C::kSmemQ + C::kSmemKV + C::kXchgBytes + 256);
+  uint32_t* s_trace = reinterpret_cast<uint32_t*>(smem + C::kSmemQ + C::kSmemKV + C::kExt2Bytes + C::kXchgBytes + 256);
   if (trace_cta())
     for (int i = threadIdx.x; i < kTrEv * kTrSteps; i += blockDim.x) s_trace[i] = 0;
 #endif
@@ -512,7 +522,23 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
   if constexpr (kExt) {
     const float sx = v.alibi[hq] / v.scale;
     ext_on = kF16 ? fabsf(sx) < 256.f : fabsf(sx) < 1e30f;
-    for (int ti = threadIdx.x; ext_on && ti < 2 * BM; ti += blockDim.x) {
+    if constexpr (D == 128) {
+      const float hi = round16<kF16>(sx), mid = round16<kF16>(sx - hi), lo = round16<kF16>(sx - hi - mid);
+      for (int ti = threadIdx.x; ext_on && ti < BM + 32; ti += blockDim.x) {
+        if (ti < BM) {   // B_ext row c = (c, c, c, 0, 0, 0, 0, 0): group c / 8, row c % 8 of its core matrix
+          const float c = (float)ti;
+          *reinterpret_cast<uint4*>(sExt + 512 + (ti >> 3) * 128 + (ti & 7) * 16) =
+              make_uint4(pack2<kF16>(c, c), pack2<kF16>(c, 0.f), 0u, 0u);
+        } else {         // A_ext(+-s): core matrix K 0..7 = 8 rows (s_hi, s_mid, s_lo, 0 ...), K 8..15 = 0
+          const int u = (ti - BM) >> 4, k = (ti - BM) & 15;
+          const float sg = u ? -1.f : 1.f;
+          *reinterpret_cast<uint4*>(sExt + u * 256 + k * 16) =
+              k < 8 ? make_uint4(pack2<kF16>(sg * hi, sg * mid), pack2<kF16>(sg * lo, 0.f), 0u, 0u)
+                    : make_uint4(0u, 0u, 0u, 0u);
+        }
+      }
+    }
+    for (int ti = threadIdx.x; D == 64 && ext_on && ti < 2 * BM; ti += blockDim.x) {
       // Row r of A_ext(+-s) = (s_hi, s_mid, s_lo, 0, ...): s split into three 16-bit parts;
       // row c of B_ext = (c, c, c, 0, ...) (c <= 127: exact).  K-major, 128-B swizzle.
       const int r = ti & (BM - 1);
@@ -639,9 +665,14 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
         if constexpr (kExt) {
           if (ext_on) {
             const int cls = ext_class(s, v, row0 + t * BM, J(j));
-            const uint32_t sa = smem_u32(sExt + (cls < 0 ? C::kExtTileBytes : 0));
-            mma_ss_warp(tS[t], smem_desc_sw128(sa, 16, 1024), smem_desc_sw128(smem_u32(sExt + 2 * C::kExtTileBytes), 16, 1024),
-                        idesc_qk, 1u);
+            if constexpr (D == 64) {
+              const uint32_t sa = smem_u32(sExt + (cls < 0 ? C::kExtTileBytes : 0));
+              mma_ss_warp(tS[t], smem_desc_sw128(sa, 16, 1024),
+                          smem_desc_sw128(smem_u32(sExt + 2 * C::kExtTileBytes), 16, 1024), idesc_qk, 1u);
+            } else {
+              const uint32_t sa = smem_u32(sExt + (cls < 0 ? 256 : 0));
+              mma_ss_warp(tS[t], smem_desc_nosw(sa, 128, 0), smem_desc_nosw(smem_u32(sExt + 512), 0, 128), idesc_qk, 1u);
+            }
           }
         }
         mma_commit_warp(&s_full[t]);
@@ -1492,6 +1523,7 @@ template <int D, bool kAlibi, bool kSoftcap, bool kF16>
 cudaError_t launch_t(const FwdTcArgs& a, cudaStream_t stream) {
   constexpr int NT = D == 128 ? ATTN_NT128 : ATTN_NT64;
   using C = Cfg<D, alibi_mma<D, kAlibi && !kSoftcap>(), NT>;
+  static_assert(C::kSmemBytes <= 232448, "shared memory");
   if constexpr (D == 128 && NT == 2 && C::kPS && kHalves == 1 && !kTraceBuild) {
     const bool pure_causal = a.v.causal && a.v.window_left < 0 && a.v.window_right < 0;
     // (ALiBi stays on the grid kernel: it walks the KV tiles diagonal-first, see J in fwd_tc_kernel)

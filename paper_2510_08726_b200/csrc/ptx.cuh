@@ -262,6 +262,16 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t start, uint32_t lbo
   d |= 2ull << 61;  // SWIZZLE_128B
   return d;
 }
+// Shared-memory matrix descriptor, no swizzle, K-major: core matrices of 8 rows x 16 B stored
+// contiguously (128 B); lbo = byte stride between core matrices along K, sbo = along M/N.
+__device__ __forceinline__ uint64_t smem_desc_nosw(uint32_t start, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((start >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+  d |= 1ull << 46;  // descriptor version (sm_100); layout type 0 = SWIZZLE_NONE
+  return d;
+}
 // Instruction descriptor for kind::f16 with fp16 (fmt 0) or bf16 (fmt 1) A/B and fp32 D.
 __host__ __device__ constexpr uint32_t idesc_f16_f32(uint32_t M, uint32_t N, uint32_t a_mn, uint32_t b_mn,
                                                      bool bf16) {
