@@ -184,19 +184,17 @@ struct Cfg {
 #ifdef ATTN_TRACE
   static constexpr int kStages = kPS ? 3 : ((D == 128) ? 4 : 8);   // room for the trace
 #else
-  static constexpr int kStages = NT == 1 ? ((D == 128) ? 2 : (kExt ? 3 : (kPS ? 4 : ATTN_NT1_STAGES64)))
-                                          : kPS ? ((D == 128) ? 3 : 6) : ((D == 128) ? 5 : (kExt ? 8 : ATTN_D64_STAGES));
+  static constexpr int kStages = NT == 1 ? ((D == 128) ? 2 : (kPS ? 4 : ATTN_NT1_STAGES64))
+                                          : kPS ? ((D == 128) ? 3 : 6) : ((D == 128) ? 5 : ATTN_D64_STAGES);
 #endif
   // Load-group barriers (ring).  The producer can be at most kStages/2 groups
   // ahead of the issuer's wait, so kStages/2 + 1 barriers never alias a phase.
   static constexpr int kPairBars = kStages / 2 + 1;
-  static constexpr int kExtTileBytes = BM * 128;                     // one 128-B swizzle atom wide
-  static constexpr int kExtBytes = (kExt && D == 64) ? 3 * kExtTileBytes : 0;     // A_ext(+s), A_ext(-s), B_ext
-  // D = 128: the tiles above leave only 3 KB, so the operands go after the K/V ring without
-  // swizzle: A_ext(+-s) 2 x 256 B (two K core matrices, all 128 rows aliased by SBO = 0) and
-  // B_ext 2 KB (16 row groups; its K 8..15 half aliases K 0..7 by LBO = 0 and meets zeros in A).
-  static constexpr int kExt2Bytes = (kExt && D == 128) ? 2 * 256 + 2048 : 0;
-  static constexpr int kSmemQ = NT * kQTileBytes + NT * kPTileBytes + kExtBytes;   // Q, P, ext tiles
+  // ALiBi-in-contraction operands, after the K/V ring, no swizzle: A_ext(+-s) 2 x 256 B (two
+  // K core matrices, all 128 rows aliased by SBO = 0) and B_ext 2 KB (16 row groups; its K 8..15
+  // half aliases K 0..7 by LBO = 0 and meets zeros in A).  (The D = 128 two-tile CTA has 3 KB left.)
+  static constexpr int kExt2Bytes = kExt ? 2 * 256 + 2048 : 0;
+  static constexpr int kSmemQ = NT * kQTileBytes + NT * kPTileBytes;   // Q, P tiles
   static constexpr int kSmemKV = kStages * kKVTileBytes;
   static constexpr int kNumBars = 1 + 2 * kStages + 6;
   static constexpr int kXchgBytes = kHalves > 1 ? 2 * kHalves * BM * 4 : 0;   // [tile][half][row] floats
@@ -427,8 +425,7 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
   uint8_t* smem = smem_raw;
   uint8_t* sQ = smem;
   uint8_t* sP = smem + NT * C::kQTileBytes;   // kPSmem: P_t, K-major SW128 [key atom][row][128 B]
-  // kExt: A_ext(+s), A_ext(-s), B_ext (D = 64: swizzled tiles after Q; D = 128: after the ring)
-  uint8_t* sExt = D == 64 ? smem + NT * C::kQTileBytes + NT * C::kPTileBytes : smem + C::kSmemQ + C::kSmemKV;
+  uint8_t* sExt = smem + C::kSmemQ + C::kSmemKV;   // kExt: A_ext(+s), A_ext(-s), B_ext
   uint8_t* sKV = smem + C::kSmemQ;
   float* xchg = reinterpret_cast<float*>(sKV + C::kSmemKV + C::kExt2Bytes);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::kSmemKV + C::kExt2Bytes + C::kXchgBytes);
@@ -522,41 +519,22 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
   if constexpr (kExt) {
     const float sx = v.alibi[hq] / v.scale;
     ext_on = kF16 ? fabsf(sx) < 256.f : fabsf(sx) < 1e30f;
-    if constexpr (D == 128) {
+    {
+      // B_ext row c = (c, c, c, 0, 0, 0, 0, 0) (c <= 127: exact), A_ext(+-s) rows = (s_hi, s_mid,
+      // s_lo, 0, ...) with s = slope / scale split into three 16-bit parts.
       const float hi = round16<kF16>(sx), mid = round16<kF16>(sx - hi), lo = round16<kF16>(sx - hi - mid);
       for (int ti = threadIdx.x; ext_on && ti < BM + 32; ti += blockDim.x) {
-        if (ti < BM) {   // B_ext row c = (c, c, c, 0, 0, 0, 0, 0): group c / 8, row c % 8 of its core matrix
+        if (ti < BM) {   // B_ext: group c / 8, row c % 8 of its core matrix
           const float c = (float)ti;
           *reinterpret_cast<uint4*>(sExt + 512 + (ti >> 3) * 128 + (ti & 7) * 16) =
               make_uint4(pack2<kF16>(c, c), pack2<kF16>(c, 0.f), 0u, 0u);
-        } else {         // A_ext(+-s): core matrix K 0..7 = 8 rows (s_hi, s_mid, s_lo, 0 ...), K 8..15 = 0
+        } else {         // A_ext(+-s): core matrix K 0..7 = 8 identical rows, K 8..15 = 0
           const int u = (ti - BM) >> 4, k = (ti - BM) & 15;
           const float sg = u ? -1.f : 1.f;
           *reinterpret_cast<uint4*>(sExt + u * 256 + k * 16) =
               k < 8 ? make_uint4(pack2<kF16>(sg * hi, sg * mid), pack2<kF16>(sg * lo, 0.f), 0u, 0u)
                     : make_uint4(0u, 0u, 0u, 0u);
         }
-      }
-    }
-    for (int ti = threadIdx.x; D == 64 && ext_on && ti < 2 * BM; ti += blockDim.x) {
-      // Row r of A_ext(+-s) = (s_hi, s_mid, s_lo, 0, ...): s split into three 16-bit parts;
-      // row c of B_ext = (c, c, c, 0, ...) (c <= 127: exact).  K-major, 128-B swizzle.
-      const int r = ti & (BM - 1);
-      uint4 row[2][8];
-      for (int u = 0; u < 2; ++u)
-        for (int ch = 0; ch < 8; ++ch) row[u][ch] = make_uint4(0u, 0u, 0u, 0u);
-      if (ti < BM) {
-        const float hi = round16<kF16>(sx), mid = round16<kF16>(sx - hi), lo = round16<kF16>(sx - hi - mid);
-        row[0][0] = make_uint4(pack2<kF16>(hi, mid), pack2<kF16>(lo, 0.f), 0u, 0u);
-        row[1][0] = make_uint4(pack2<kF16>(-hi, -mid), pack2<kF16>(-lo, 0.f), 0u, 0u);
-        for (int u = 0; u < 2; ++u)
-          for (int ch = 0; ch < 8; ++ch)
-            *reinterpret_cast<uint4*>(sExt + u * C::kExtTileBytes + r * 128 + ((ch ^ (r & 7)) << 4)) = row[u][ch];
-      } else {
-        const float c = (float)r;
-        row[0][0] = make_uint4(pack2<kF16>(c, c), pack2<kF16>(c, 0.f), 0u, 0u);
-        for (int ch = 0; ch < 8; ++ch)
-          *reinterpret_cast<uint4*>(sExt + 2 * C::kExtTileBytes + r * 128 + ((ch ^ (r & 7)) << 4)) = row[0][ch];
       }
     }
     fence_proxy_async_smem();   // generic-proxy stores -> tensor core reads
@@ -665,14 +643,8 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
         if constexpr (kExt) {
           if (ext_on) {
             const int cls = ext_class(s, v, row0 + t * BM, J(j));
-            if constexpr (D == 64) {
-              const uint32_t sa = smem_u32(sExt + (cls < 0 ? C::kExtTileBytes : 0));
-              mma_ss_warp(tS[t], smem_desc_sw128(sa, 16, 1024),
-                          smem_desc_sw128(smem_u32(sExt + 2 * C::kExtTileBytes), 16, 1024), idesc_qk, 1u);
-            } else {
-              const uint32_t sa = smem_u32(sExt + (cls < 0 ? 256 : 0));
-              mma_ss_warp(tS[t], smem_desc_nosw(sa, 128, 0), smem_desc_nosw(smem_u32(sExt + 512), 0, 128), idesc_qk, 1u);
-            }
+            const uint32_t sa = smem_u32(sExt + (cls < 0 ? 256 : 0));
+            mma_ss_warp(tS[t], smem_desc_nosw(sa, 128, 0), smem_desc_nosw(smem_u32(sExt + 512), 0, 128), idesc_qk, 1u);
           }
         }
         mma_commit_warp(&s_full[t]);
