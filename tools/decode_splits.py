@@ -4,7 +4,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2510_08726_b200 as pb
 
-Hq, Hkv, L, D = 32, 8, 131072, 128
+Hq, Hkv, L, D = (int(os.environ.get(k, d)) for k, d in (("HQ", 32), ("HKV", 8), ("L", 131072), ("D", 128)))
 for B in [int(x) for x in os.environ.get("BS", "1 2 4 8 16").split()]:
     q = torch.randn(B, Hq, 1, D, device="cuda", dtype=torch.bfloat16)
     k = torch.randn(B, Hkv, L, D, device="cuda", dtype=torch.bfloat16)
