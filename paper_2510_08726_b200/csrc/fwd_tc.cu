@@ -144,6 +144,9 @@ __device__ __forceinline__ bool trace_cta() { return blockIdx.x == 5 && blockIdx
 #ifndef ATTN_ALIBI_MMA
 #define ATTN_ALIBI_MMA 1
 #endif
+#ifndef ATTN_PERSIST_LPT
+#define ATTN_PERSIST_LPT 0   // measured equal (the snake already balances)
+#endif
 #ifndef ATTN_CAUSAL_L2_MB
 #define ATTN_CAUSAL_L2_MB 96
 #endif
@@ -1082,8 +1085,19 @@ __device__ __forceinline__ Unit unit_of(const Shape& s, const VariantParams& v, 
   const int nz = s.B * (s.kv_splits > 1 ? s.kv_splits : 1);
   Unit u;
   u.valid = idx < nqb * s.Hq * nz;
-  const int head_lin = idx / nqb, qi = idx % nqb;
-  u.qblk = v.causal ? nqb - 1 - qi : qi;          // heaviest causal q-block of a head first
+  int head_lin = idx / nqb, qi = idx % nqb;
+  if (v.causal && ATTN_PERSIST_LPT) {   // heaviest-first across an L2-sized group of heads (as the grid kernel)
+    const int nh = s.Hq * nz;
+    const long long kv_bytes = 4LL * s.Skv * 128 / (s.Hq / s.Hkv);
+    const int gh = (int)max(1LL, min((long long)nh, ((long long)ATTN_CAUSAL_L2_MB << 20) / max(kv_bytes, 1LL)));
+    const int grp = idx / (nqb * gh), r = idx - grp * nqb * gh;
+    const int ghe = min(gh, nh - grp * gh);
+    if (u.valid) {
+      qi = r / ghe;
+      head_lin = grp * gh + r % ghe;
+    }
+  }
+  u.qblk = v.causal ? nqb - 1 - qi : qi;          // heaviest causal q-block first
   u.hq = head_lin % s.Hq;
   u.zb = head_lin / s.Hq;
   u.b = s.kv_splits > 1 ? u.zb % s.B : u.zb;
