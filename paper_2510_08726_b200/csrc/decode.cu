@@ -343,14 +343,34 @@ __global__ void __launch_bounds__(kThreads) decode_split_kernel(const __grid_con
   for (int rho = warp; rho < nrows; rho += kConsumerWarps) {   // warp reduces row rho over the splits
     const int hh = hkv * G + rho / Sq, qi = rho % Sq;
     const long long mb = (long long)b * a.parts.m_sb + (long long)hh * a.parts.m_sh + qi;
+    // one round trip: every lane loads its splits' (m, l) pairs before any reduction
+    constexpr int kMaxPer = 8;            // splits per lane held in registers (S <= 256 here)
+    float ms[kMaxPer], ls[kMaxPer];
+#pragma unroll
+    for (int i = 0; i < kMaxPer; ++i) {
+      const int sp = lane + 32 * i;
+      ms[i] = sp < S ? __ldcg(a.parts.m + sp * a.parts.m_sp + mb) : -INFINITY;
+      ls[i] = sp < S ? __ldcg(a.parts.l + sp * a.parts.m_sp + mb) : 0.f;
+    }
     float M = -INFINITY;
-    for (int sp = lane; sp < S; sp += 32) M = fmaxf(M, __ldcg(a.parts.m + sp * a.parts.m_sp + mb));
+#pragma unroll
+    for (int i = 0; i < kMaxPer; ++i) M = fmaxf(M, ms[i]);
+    for (int sp = lane + 32 * kMaxPer; sp < S; sp += 32) M = fmaxf(M, __ldcg(a.parts.m + sp * a.parts.m_sp + mb));
 #pragma unroll
     for (int o2 = 16; o2 > 0; o2 >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o2));
     float L = 0.f;
-    for (int sp = lane; sp < S; sp += 32) {
-      const float ms = __ldcg(a.parts.m + sp * a.parts.m_sp + mb);
-      const float w = (ms == -INFINITY) ? 0.f : expf(ms - M);   // repair term exp(max_s - max_g)
+#pragma unroll
+    for (int i = 0; i < kMaxPer; ++i) {
+      const int sp = lane + 32 * i;
+      if (sp < S) {
+        const float w = (ms[i] == -INFINITY) ? 0.f : expf(ms[i] - M);   // repair term exp(max_s - max_g)
+        wts[rho * S + sp] = w;
+        L = fmaf(w, ls[i], L);
+      }
+    }
+    for (int sp = lane + 32 * kMaxPer; sp < S; sp += 32) {
+      const float m_s = __ldcg(a.parts.m + sp * a.parts.m_sp + mb);
+      const float w = (m_s == -INFINITY) ? 0.f : expf(m_s - M);
       wts[rho * S + sp] = w;
       L = fmaf(w, __ldcg(a.parts.l + sp * a.parts.m_sp + mb), L);
     }
@@ -362,18 +382,38 @@ __global__ void __launch_bounds__(kThreads) decode_split_kernel(const __grid_con
     }
   }
   named_bar_sync(1, kConsumerWarps * 32);
-  for (int e = threadIdx.x; e < nrows * D; e += kConsumerWarps * 32) {
-    const int rho = e / D, d = e % D;
+  // O = sum_s w_s O_s: one float4 of one row per thread, the splits' loads issued in batches of 8
+  for (int e4 = threadIdx.x; e4 < nrows * (D / 4); e4 += kConsumerWarps * 32) {
+    const int rho = e4 / (D / 4), d = (e4 % (D / 4)) * 4;
     const int hh = hkv * G + rho / Sq, qi = rho % Sq;
     const float L = stat[rho * 2 + 1];
     const float* po = a.parts.o + (long long)b * a.parts.o_sb + (long long)hh * a.parts.o_sh + (long long)qi * D + d;
-    float acc = 0.f;
-    if (L > 0.f)
-      for (int sp = 0; sp < S; ++sp) acc = fmaf(wts[rho * S + sp], __ldcg(po + sp * a.parts.o_sp), acc);
-    const float out = L > 0.f ? acc / L : 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (L > 0.f) {
+      for (int s0 = 0; s0 < S; s0 += 8) {
+        float4 ov[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          ov[i] = s0 + i < S ? __ldcg(reinterpret_cast<const float4*>(po + (long long)(s0 + i) * a.parts.o_sp))
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float w = s0 + i < S ? wts[rho * S + s0 + i] : 0.f;
+          acc.x = fmaf(w, ov[i].x, acc.x);
+          acc.y = fmaf(w, ov[i].y, acc.y);
+          acc.z = fmaf(w, ov[i].z, acc.z);
+          acc.w = fmaf(w, ov[i].w, acc.w);
+        }
+      }
+    }
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    const float out[4] = {acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv};
     const long long oi = (long long)b * a.o_sb + (long long)hh * a.o_sh + (long long)qi * a.o_ss + d;
-    if (a.out_f16) reinterpret_cast<__half*>(a.o)[oi] = __float2half_rn(out);
-    else reinterpret_cast<__nv_bfloat16*>(a.o)[oi] = __float2bfloat16_rn(out);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (a.out_f16) reinterpret_cast<__half*>(a.o)[oi + c] = __float2half_rn(out[c]);
+      else reinterpret_cast<__nv_bfloat16*>(a.o)[oi + c] = __float2bfloat16_rn(out[c]);
+    }
     if (d == 0 && a.lse) a.lse[((long long)b * a.s.Hq + hh) * Sq + qi] = L > 0.f ? stat[rho * 2] + logf(L) : -INFINITY;
   }
   if (threadIdx.x == 0) *ticket = 0u;     // ready for the next call
