@@ -350,9 +350,42 @@ __device__ __forceinline__ float row_max_pass(float (&x)[N], int rel_lo, int rel
 // log2 domain used by the exponentials; returns the row max of the tile.
 // Plain variant: x stays raw (scale folded into the exp FFMA) and the max is
 // rescaled afterwards (scale > 0 so max commutes with it).
+#ifndef ATTN_TANH_POLY
+#define ATTN_TANH_POLY 0   // softcap tanh on the FMA pipe for every N-th column (measured: N = 2 -10 %, 3 equal; off)
+#endif
+// tanh(y) for |y| <= 1/2 by its odd Taylor polynomial to y^7 (truncation < 4.3e-5 absolute,
+// below tanh.approx.f32's ~2^-11 relative error): 5 FMA-pipe operations instead of one MUFU op.
+__device__ __forceinline__ float tanh_poly_small(float y) {
+  const float y2 = y * y;
+  float p = fmaf(y2, -17.f / 315.f, 2.f / 15.f);
+  p = fmaf(y2, p, -1.f / 3.f);
+  return fmaf(y * y2, p, y);
+}
+
 template <bool kAlibi, bool kSoftcap, bool kMask, bool kChunked = true, int N>
 __device__ __forceinline__ float score_tile(float (&x)[N], const VariantParams& v, float nslope2, float dq0,
                                             int rel_lo, int rel_hi) {
+  if constexpr (kSoftcap && ATTN_TANH_POLY > 0) {
+    // Softcap spends two SFU ops per element (tanh, then ex2) and is MUFU-bound.  When every
+    // |y| = |x / cap| of the warp's tile is <= 1/2 (the usual regime: logits well below the
+    // cap), every ATTN_TANH_POLY-th column evaluates tanh on the FMA pipe instead.
+    float ya = 0.f;
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      x[c] *= v.scale_over_cap;
+      ya = fmaxf(ya, fabsf(x[c]));
+    }
+    auto fin = [&](float t, int c) {
+      float xv = v.softcap_log2 * t;                                        // R3: cap * tanh(x / cap)
+      if constexpr (kAlibi) xv = fmaf(nslope2, fabsf(dq0 - (float)c), xv);  // R4
+      return xv;
+    };
+    if (__all_sync(0xffffffffu, ya <= 0.5f))
+      return row_max_pass<kMask, kChunked>(x, rel_lo, rel_hi, [&](float y, int c) {
+        return fin(c % ATTN_TANH_POLY == ATTN_TANH_POLY - 1 ? tanh_poly_small(y) : tanh_approx(y), c);
+      });
+    return row_max_pass<kMask, kChunked>(x, rel_lo, rel_hi, [&](float y, int c) { return fin(tanh_approx(y), c); });
+  }
   float mt = row_max_pass<kMask, kChunked>(x, rel_lo, rel_hi, [&](float xv, int c) {
     if constexpr (kSoftcap) {
       xv = v.softcap_log2 * tanh_approx(xv * v.scale_over_cap);   // R3: cap * tanh(x / cap)

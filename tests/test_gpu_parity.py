@@ -93,6 +93,9 @@ VARIANTS = {
     # the diagonal take different paths (fwd_tc.cu ext_class)
     "alibi": dict(alibi=True),
     "alibi_band": dict(alibi=True, window_left=150, window_right=21),
+    # cap 8: |x / cap| <= 1/2 for most warps (tanh on the FMA pipe for every other column),
+    # above it for some (all on the SFU) -- both paths in one launch
+    "softcap8_causal": dict(causal=True, softcap=8.0),
 }
 
 
@@ -233,6 +236,7 @@ FULL = {
     "variants_alibi": dict(cid=4, B=8, Hq=16, Hkv=16, S=2048, D=64, alibi=True),
     "mha_alibi_causal": dict(cid=2, B=8, Hq=16, Hkv=16, S=4096, D=128, causal=True, alibi=True),
     "variants_softcap_causal": dict(cid=4, B=8, Hq=16, Hkv=16, S=2048, D=64, causal=True, softcap=2.0),
+    "variants_softcap50_causal": dict(cid=4, B=8, Hq=16, Hkv=16, S=2048, D=64, causal=True, softcap=50.0),
 }
 
 
@@ -476,7 +480,8 @@ def test_device_generator_fp16_is_bit_identical():
 
 
 @pytest.mark.parametrize("D", [128, 64])
-@pytest.mark.parametrize("name", ["global", "causal", "alibi_causal", "softcap_causal", "window_band", "alibi"])
+@pytest.mark.parametrize("name", ["global", "causal", "alibi_causal", "softcap_causal", "window_band", "alibi",
+                                  "softcap8_causal"])
 def test_fp16_prefill_small(name, D):
     kw = dict(VARIANTS[name])
     B, Hq, Hkv, S = 1, 4, 2, 300
