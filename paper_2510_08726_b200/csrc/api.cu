@@ -290,6 +290,11 @@ int32_t attn_splitkv_default_splits(const attn_problem* p, int32_t sm_count) {
   // (tools/decode_splits.py) this streams K/V fastest (B = 1..16: 6.2-7.2 TB/s), while two
   // per SM or a partial second wave lose 5-20 %.
   int64_t splits = sm_count / units;
+  // With >= 64 (b, hkv) groups the floor leaves SMs idle (B = 8: 128 of 148; B = 16: 128) while
+  // two decode CTAs fit per SM, so round UP (<= 2 per SM, all resident): measured r1k
+  // (profiles/r1k_decode_splits.txt) B = 8 6954 -> 7131, B = 16 6974 -> 7146 GB/s; below 64
+  // groups rounding up loses (B = 1: 6352 -> 6088, B = 2: 6783 -> 6536, B = 4: 6869 -> 6795).
+  if (units >= 64 && units < sm_count) splits = (sm_count + units - 1) / units;
   const int64_t max_splits = (p->seqlen_kv + nk - 1) / nk;
   if (splits > max_splits) splits = max_splits;
   if (splits < 1) splits = 1;
