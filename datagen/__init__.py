@@ -121,6 +121,42 @@ def as_f64(x: np.ndarray, dtype: str) -> np.ndarray:
     return np.asarray(x, dtype=np.float32).astype(np.float64)
 
 
+def _to_dtype(x32: np.ndarray, dtype: str) -> np.ndarray:
+    if dtype == "bf16":
+        return f32_to_bf16_bits(x32)
+    if dtype == "f16":
+        return x32.astype(np.float16).view(np.uint16)
+    return x32.astype(np.float32)
+
+
+def rising_rows(n: int) -> np.ndarray:
+    """Rows that get the rising component in ``rising_logits`` (an irregular ~half of them,
+    so a warp of 32 rows mixes rows that need the repair with rows that do not)."""
+    i = np.arange(n, dtype=np.int64)
+    return ((i * 37) >> 4) & 1 == 1
+
+
+def rising_logits(q: np.ndarray, k: np.ndarray, dtype: str, amp: float, rate: float, tile: int = 128,
+                  descending: bool = False):
+    """Adversarial inputs for the repair tests: copies of generated q, k
+    ([..., S, D], bits or fp32) with coordinate 0 replaced by
+        q[..., i, 0] = amp if rising_rows(Sq)[i] else 0,
+        k[..., j, 0] = rate * j / tile         (descending: rate * (Skv - 1 - j) / tile),
+    each rounded to ``dtype``.  So q_i . k_j rises by about amp * rate along every `tile`
+    keys of the ascending (or descending) KV walk and the running max of a rising row jumps
+    by that much per KV tile.  No attention arithmetic: only the input values change."""
+    q2, k2 = np.array(q, copy=True), np.array(k, copy=True)
+    sq, skv = q.shape[-2], k.shape[-2]
+    qa = np.where(rising_rows(sq), np.float32(amp), np.float32(0.0)).astype(np.float32)
+    j = np.arange(skv, dtype=np.float64)
+    if descending:
+        j = (skv - 1) - j
+    ka = (np.float64(rate) * j / tile).astype(np.float32)
+    q2[..., 0] = _to_dtype(qa, dtype)
+    k2[..., 0] = _to_dtype(ka, dtype)
+    return q2, k2
+
+
 def alibi_slopes(heads: int) -> np.ndarray:
     """Standard ALiBi slopes 2^(-8(h+1)/H), fp32."""
     h = np.arange(heads, dtype=np.float64)

@@ -51,3 +51,20 @@ def to_device(x: np.ndarray, device="cuda", dtype: str = "bf16") -> torch.Tensor
         tdt = torch.float16 if dtype == "f16" else torch.bfloat16
         return torch.from_numpy(x.view(np.int16).copy()).view(tdt).to(device)
     return torch.from_numpy(np.ascontiguousarray(x)).to(device)
+
+
+def rising_logits_(q: torch.Tensor, k: torch.Tensor, amp: float, rate: float, tile: int = 128,
+                   descending: bool = False):
+    """In-place device twin of ``datagen.rising_logits`` (bit-identical values)."""
+    from . import rising_rows
+    sq, skv = q.shape[-2], k.shape[-2]
+    rows = torch.from_numpy(rising_rows(sq)).to(q.device)
+    qa = torch.where(rows, torch.tensor(amp, dtype=torch.float32, device=q.device),
+                     torch.tensor(0.0, dtype=torch.float32, device=q.device))
+    j = torch.arange(skv, dtype=torch.float64, device=k.device)
+    if descending:
+        j = (skv - 1) - j
+    ka = (float(rate) * j / tile).to(torch.float32)
+    q[..., 0] = qa.to(q.dtype)
+    k[..., 0] = ka.to(k.dtype)
+    return q, k

@@ -308,6 +308,24 @@ ATTN_API int attn_abi_version(void);
  * launch accounting in bench.py). */
 ATTN_API int attn_last_launch_count(void);
 
+/* Repair-event counters (test instrumentation; proves that the Eq. 7 O-rescale,
+ * P:604-607, h = exp(r - r') t of Fig. 18d, runs in a given kernel).
+ * counters: DEVICE uint32 [ATTN_REPAIR_SLOTS], caller-owned, or NULL (off, the
+ * default).  The setting is thread-local and applies to every later call on the
+ * calling thread: each warp that rescales its O accumulator by a factor < 1
+ * adds 1 to counters[slot] once per KV step, slot = the kernel that ran:
+ *   ATTN_REPAIR_FWD128  prefill grid kernel, D = 128   (fwd_tc_kernel)
+ *   ATTN_REPAIR_FWD64   prefill grid kernel, D = 64    (fwd_tc_kernel, 2 CTAs/SM)
+ *   ATTN_REPAIR_PERSIST persistent causal prefill kernel (fwd_tc_persist_kernel)
+ *   ATTN_REPAIR_DECODE  split-KV decode local section  (decode_split_kernel)
+ * Off, it costs nothing; on, one atomic per warp inside the rescale branch. */
+#define ATTN_REPAIR_FWD128 0
+#define ATTN_REPAIR_FWD64 1
+#define ATTN_REPAIR_PERSIST 2
+#define ATTN_REPAIR_DECODE 3
+#define ATTN_REPAIR_SLOTS 4
+ATTN_API void attn_debug_repair_counters(unsigned int* counters);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,7 +21,7 @@ from . import _ffi
 from ._ffi import AttnParts, AttnProblem, AttnTensor, check, load
 
 __all__ = ["fused_fwd", "splitkv_decode", "combine", "merge_partials", "softmax_rows", "default_splits", "workspace_bytes",
-           "last_launch_count", "Parts", "load"]
+           "last_launch_count", "Parts", "load", "repair_counters"]
 
 _DT = {torch.bfloat16: _ffi.ATTN_BF16, torch.float32: _ffi.ATTN_FP32, torch.float16: _ffi.ATTN_FP16}
 
@@ -63,6 +63,30 @@ def _problem(q, k, *, scale, causal, window, alibi_slopes, softcap, q_pos_offset
 def last_launch_count() -> int:
     """Kernels enqueued by the last successful call on this thread."""
     return load().attn_last_launch_count()
+
+
+class repair_counters:
+    """Context manager around ``attn_debug_repair_counters``: while active, the
+    kernels count the warps that apply the Eq. 7 O-rescale into a
+    device uint32 tensor of ``ATTN_REPAIR_SLOTS`` slots (test instrumentation).
+    ``counts()`` reads them: a dict kernel name -> events."""
+
+    NAMES = ("fwd128", "fwd64", "persist", "decode")
+
+    def __init__(self, device="cuda"):
+        self.buf = torch.zeros(_ffi.ATTN_REPAIR_SLOTS, dtype=torch.int32, device=device)
+
+    def __enter__(self):
+        load().attn_debug_repair_counters(self.buf.data_ptr())
+        return self
+
+    def __exit__(self, *exc):
+        load().attn_debug_repair_counters(None)
+        return False
+
+    def counts(self) -> dict:
+        torch.cuda.synchronize(self.buf.device)
+        return dict(zip(self.NAMES, (int(x) for x in self.buf.cpu())))
 
 
 def fused_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: Optional[float] = None,

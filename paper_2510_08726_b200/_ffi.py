@@ -26,7 +26,11 @@ EXPORTED = ("attn_fused_fwd", "attn_splitkv_default_splits", "attn_splitkv_works
             "attn_abi_version", "attn_last_launch_count", "attn_merge_partials", "attn_softmax_rows",
             "attn_nccl_get_unique_id", "attn_nccl_comm_init", "attn_nccl_comm_destroy",
             "attn_decode_kv_sharded_workspace_bytes", "attn_decode_kv_sharded",
-            "attn_fused_fwd_default_splits", "attn_fused_fwd_workspace_bytes", "attn_fused_fwd_splitkv")
+            "attn_fused_fwd_default_splits", "attn_fused_fwd_workspace_bytes", "attn_fused_fwd_splitkv",
+            "attn_debug_repair_counters")
+# repair-event counter slots (include/attn.h ATTN_REPAIR_*)
+ATTN_REPAIR_FWD128, ATTN_REPAIR_FWD64, ATTN_REPAIR_PERSIST, ATTN_REPAIR_DECODE = 0, 1, 2, 3
+ATTN_REPAIR_SLOTS = 4
 
 
 class AttnTensor(ctypes.Structure):
@@ -101,6 +105,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.attn_last_error.restype = ctypes.c_char_p
     lib.attn_abi_version.restype = ctypes.c_int
     lib.attn_last_launch_count.restype = ctypes.c_int
+    lib.attn_debug_repair_counters.argtypes = [vp]
+    lib.attn_debug_repair_counters.restype = None
     if lib.attn_abi_version() != 1:
         raise RuntimeError("libattn.so ABI version mismatch")
     _lib = lib

@@ -21,6 +21,7 @@ namespace {
 
 thread_local char g_err[512] = "";
 thread_local int g_launches = 0;
+thread_local unsigned* g_repair_events = nullptr;   // attn_debug_repair_counters
 
 attn_status fail(attn_status s, const char* fmt, ...) {
   va_list ap;
@@ -115,6 +116,7 @@ attn_status check_problem(const attn_problem* p, attn::VariantParams* vp) {
   vp->window_right = p->window_right;
   vp->q_off = qoff;
   vp->kv_off = p->kv_pos_offset;
+  vp->repair_events = g_repair_events;
   return ATTN_OK;
 }
 
@@ -145,6 +147,7 @@ extern "C" {
 int attn_abi_version(void) { return ATTN_ABI_VERSION; }
 const char* attn_last_error(void) { return g_err; }
 int attn_last_launch_count(void) { return g_launches; }
+void attn_debug_repair_counters(unsigned int* counters) { g_repair_events = counters; }
 
 const char* attn_status_string(attn_status s) {
   switch (s) {

@@ -232,6 +232,9 @@ __global__ void __launch_bounds__(kThreads) decode_split_kernel(const __grid_con
     const float a_lo = row_step(s4, 0, qpos_lo, jlo_lo, jhi_lo, ns_lo, ok_lo, key0, m_lo, l_lo, p_lo);
     float a_hi = 1.f;
     if constexpr (kHi) a_hi = row_step(s4, 2, qpos_hi, jlo_hi, jhi_hi, ns_hi, ok_hi, key0, m_hi, l_hi, p_hi);
+    if (v.repair_events != nullptr &&   // test instrumentation: a live O accumulator rescaled by < 1
+        __any_sync(0xffffffffu, (a_lo > 0.f && a_lo < 1.f) || (a_hi > 0.f && a_hi < 1.f)) && lane == 0)
+      atomicAdd(v.repair_events + 3, 1u);
 #pragma unroll
     for (int n = 0; n < D / 8; ++n) {
       o[n][0] *= a_lo;

@@ -993,6 +993,7 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
       // (done after P so the S registers are dead; PV(j) cannot start before P is ready)
       if (__any_sync(0xffffffffu, need_o)) {
         // O = h(O): wait for PV of the previous tile, then rescale this thread's O columns.
+        if (v.repair_events != nullptr && lane == 0) atomicAdd(v.repair_events + (D == 64 ? 1 : 0), 1u);
         mbar_wait(&o_done[t], (it - 1) & 1);
         tc_fence_after();
 #pragma unroll
@@ -1458,6 +1459,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         if (__any_sync(0xffffffffu, need_o)) {   // O = h(O) (rare: lazy repair, R9)
+          if (v.repair_events != nullptr && lane == 0) atomicAdd(v.repair_events + 2, 1u);
 #pragma unroll
           for (int c = 0; c < D / 32; ++c) {
             uint32_t o[32];

@@ -35,6 +35,7 @@ struct VariantParams {
   int window_left, window_right;
   long long q_off;      // absolute position of query row 0
   long long kv_off;     // absolute position of local key 0
+  unsigned* repair_events;   // nullable [ATTN_REPAIR_SLOTS] (attn_debug_repair_counters)
 };
 
 struct Shape {

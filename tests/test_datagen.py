@@ -47,3 +47,22 @@ def test_bf16_rounding_matches_torch():
     np.testing.assert_array_equal(ours, ref)
     np.testing.assert_array_equal(datagen.bf16_bits_to_f32(ours),
                                   torch.from_numpy(x).to(torch.bfloat16).float().numpy())
+
+
+def test_rising_logits_shape_and_growth():
+    """The repair-test inputs: coordinate 0 only, q amplitude on rising_rows, k a ramp of
+    `rate` per `tile` keys (ascending or descending), values exactly representable."""
+    q = datagen.tensor(3, 1, (1, 2, 300, 64))
+    k = datagen.tensor(3, 2, (1, 1, 700, 64))
+    q2, k2 = datagen.rising_logits(q, k, "bf16", 8.0, 8.0)
+    assert np.array_equal(q2[..., 1:], q[..., 1:]) and np.array_equal(k2[..., 1:], k[..., 1:])
+    qa = datagen.as_f64(q2, "bf16")[0, 0, :, 0]
+    rows = datagen.rising_rows(300)
+    assert 0.3 < rows.mean() < 0.7
+    assert np.all(qa[rows] == 8.0) and np.all(qa[~rows] == 0.0)
+    ka = datagen.as_f64(k2, "bf16")[0, 0, :, 0]
+    assert ka[0] == 0.0 and abs(ka[128] - 8.0) < 1e-9 and abs(ka[512] - 32.0) < 1e-9
+    assert np.all(np.diff(ka) >= 0)
+    _, kd = datagen.rising_logits(q, k, "bf16", 8.0, 8.0, descending=True)
+    kda = datagen.as_f64(kd, "bf16")[0, 0, :, 0]
+    assert kda[-1] == 0.0 and np.all(np.diff(kda) <= 0)
