@@ -145,7 +145,7 @@ ATTN_API attn_status attn_fused_fwd(const attn_problem* prob, attn_tensor q, att
  * NORMALISED partial (O_s, lse_s) -- the repaired triple (m = lse_s, l = 1,
  * O_s) of Thm. 2 -- into the workspace; Eq. 8 then merges the
  * splits into o / lse.  Exact in real arithmetic for any split (Eq. 4); the
- * partial O is rounded to q's dtype once before the merge.
+ * partials stay fp32, so the output is rounded once (by the merge).
  *
  * attn_fused_fwd_default_splits: min(sm_count / units, n_kv_tiles / 4, 16)
  *   with units = B * Hq * ceil(s_q / 256) and 128-key tiles, or 1 when that is
@@ -163,6 +163,22 @@ ATTN_API size_t attn_fused_fwd_workspace_bytes(const attn_problem* prob, int32_t
 ATTN_API attn_status attn_fused_fwd_splitkv(const attn_problem* prob, attn_tensor q, attn_tensor k, attn_tensor v,
                                             attn_tensor o, float* lse, int32_t num_splits, void* workspace,
                                             size_t workspace_bytes, attn_stream_t stream);
+
+/* ---------------------------------------------------------------------
+ * attn_fused_fwd_partial -- Rolling Update over a KV SHARD with the result kept
+ * as an fp32 normalised partial, for context-parallel prefill (each GPU holds
+ * keys [kv_pos_offset, kv_pos_offset + seqlen_kv) of a longer sequence; the
+ * per-GPU partials are merged with attn_merge_partials, Eq. 8).
+ * A normalised partial (O_r, lse_r) is the repaired triple (m = lse_r, l = 1,
+ * O_r) of Thm. 2, so keeping O_r in fp32 leaves one rounding (the merge's) in
+ * the final output.
+ *   q/k/v as attn_fused_fwd (bf16 or fp16, D in {64, 128});
+ *   o_part: DEVICE fp32 [B][Hq][Sq][D] contiguous, 16-byte aligned (required);
+ *   lse   : DEVICE fp32 [B][Hq][Sq] contiguous (required).
+ * One launch.  Errors: those of attn_fused_fwd; UNSUPPORTED for fp32 inputs.
+ * ------------------------------------------------------------------- */
+ATTN_API attn_status attn_fused_fwd_partial(const attn_problem* prob, attn_tensor q, attn_tensor k, attn_tensor v,
+                                            float* o_part, float* lse, attn_stream_t stream);
 
 /* ---------------------------------------------------------------------
  * Split-K Update decode (Alg. 2, Fig. 5): dtype bf16 or fp16, D in {64, 128},

@@ -20,7 +20,7 @@ import torch
 from . import _ffi
 from ._ffi import AttnParts, AttnProblem, AttnTensor, check, load
 
-__all__ = ["fused_fwd", "splitkv_decode", "combine", "merge_partials", "softmax_rows", "default_splits", "workspace_bytes",
+__all__ = ["fused_fwd", "fused_fwd_partial", "splitkv_decode", "combine", "merge_partials", "softmax_rows", "default_splits", "workspace_bytes",
            "last_launch_count", "Parts", "load", "repair_counters"]
 
 _DT = {torch.bfloat16: _ffi.ATTN_BF16, torch.float32: _ffi.ATTN_FP32, torch.float16: _ffi.ATTN_FP16}
@@ -37,6 +37,33 @@ def _as_tensor(t: Optional[torch.Tensor]) -> AttnTensor:
 def _stream(stream) -> ctypes.c_void_p:
     s = torch.cuda.current_stream() if stream is None else stream
     return ctypes.c_void_p(s.cuda_stream)
+
+
+def _check_io(q, k, v, out=None, lse=None, lse_shape=None):
+    """Shape / dtype / device checks the C ABI cannot make (it sees only pointers and
+    strides, not allocation sizes): a mismatch here would be an out-of-bounds device
+    access, so it raises ValueError before anything is launched."""
+    for name, t in (("q", q), ("k", k), ("v", v)):
+        if t.dim() != 4:
+            raise ValueError(f"{name} must be a [B, H, S, D] tensor (got {tuple(t.shape)})")
+    if v.shape != k.shape:
+        raise ValueError(f"v {tuple(v.shape)} must have k's shape {tuple(k.shape)}")
+    if k.shape[0] != q.shape[0] or k.shape[3] != q.shape[3]:
+        raise ValueError("q and k disagree on batch or head_dim")
+    if k.shape[1] < 1 or q.shape[1] % k.shape[1] != 0:
+        raise ValueError(f"heads_q ({q.shape[1]}) must be a multiple of heads_kv ({k.shape[1]})")
+    for name, t in (("k", k), ("v", v)) + ((("out", out),) if out is not None else ()):
+        if t.dtype != q.dtype:
+            raise ValueError(f"{name} dtype {t.dtype} differs from q's {q.dtype}")
+        if t.device != q.device:
+            raise ValueError(f"{name} is on {t.device}, q on {q.device}")
+    if out is not None and out.shape != q.shape:
+        raise ValueError(f"out {tuple(out.shape)} must have q's shape {tuple(q.shape)}")
+    if lse is not None:
+        if lse.dtype != torch.float32 or not lse.is_contiguous() or lse.device != q.device:
+            raise ValueError("lse must be a contiguous float32 tensor on q's device")
+        if tuple(lse.shape) != tuple(lse_shape):
+            raise ValueError(f"lse must have shape {tuple(lse_shape)} (got {tuple(lse.shape)})")
 
 
 def _problem(q, k, *, scale, causal, window, alibi_slopes, softcap, q_pos_offset, kv_pos_offset,
@@ -114,8 +141,7 @@ def fused_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: Optio
         out = torch.empty_like(q, memory_format=torch.contiguous_format)
     if return_lse and lse is None:
         lse = torch.empty(q.shape[:3], device=q.device, dtype=torch.float32)
-    if lse is not None and (not lse.is_contiguous() or lse.dtype != torch.float32):
-        raise ValueError("lse must be a contiguous float32 [B, Hq, Sq] tensor")
+    _check_io(q, k, v, out, lse, q.shape[:3])
     splits = kv_splits if kv_splits > 0 else lib.attn_fused_fwd_default_splits(ctypes.byref(prob), 0)
     if splits <= 1:
         check(lib.attn_fused_fwd(ctypes.byref(prob), _as_tensor(q), _as_tensor(k), _as_tensor(v), _as_tensor(out),
@@ -129,17 +155,48 @@ def fused_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: Optio
     return (out, lse) if return_lse else out
 
 
+def fused_fwd_partial(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: Optional[float] = None,
+                      causal: bool = False, window: Tuple[int, int] = (-1, -1),
+                      alibi_slopes: Optional[torch.Tensor] = None, softcap: float = 0.0,
+                      q_pos_offset: Optional[int] = None, kv_pos_offset: int = 0,
+                      seqlen_kv_total: Optional[int] = None, out: Optional[torch.Tensor] = None,
+                      lse: Optional[torch.Tensor] = None, stream=None):
+    """Rolling Update over a KV shard kept as an fp32 normalised partial
+    (``attn_fused_fwd_partial``): returns (O_r fp32 [B, Hq, Sq, D], lse_r fp32 [B, Hq, Sq]),
+    merged across shards by :func:`merge_partials` (context-parallel prefill)."""
+    lib = load()
+    prob = _problem(q, k, scale=scale, causal=causal, window=window, alibi_slopes=alibi_slopes, softcap=softcap,
+                    q_pos_offset=q_pos_offset, kv_pos_offset=kv_pos_offset, seqlen_kv_total=seqlen_kv_total)
+    if out is None:
+        out = torch.empty(q.shape, dtype=torch.float32, device=q.device)
+    if lse is None:
+        lse = torch.empty(q.shape[:3], dtype=torch.float32, device=q.device)
+    _check_io(q, k, v, None, lse, q.shape[:3])
+    if out.dtype != torch.float32 or tuple(out.shape) != tuple(q.shape) or not out.is_contiguous() \
+            or out.device != q.device:
+        raise ValueError("out must be a contiguous float32 tensor of q's shape")
+    check(lib.attn_fused_fwd_partial(ctypes.byref(prob), _as_tensor(q), _as_tensor(k), _as_tensor(v), out.data_ptr(),
+                                     lse.data_ptr(), _stream(stream)), "attn_fused_fwd_partial")
+    return out, lse
+
+
 _SCRATCH = {}
 
 
+def _torch_stream(device, stream):
+    return torch.cuda.current_stream(device) if stream is None else stream
+
+
 def _scratch(device, need: int, stream) -> torch.Tensor:
-    """Per-(device, stream) scratch for the split-KV prefill partials (no zeroing needed)."""
-    key = (device.index if device.index is not None else torch.cuda.current_device(), _stream(stream).value)
+    """Per-(device, stream) scratch for the split-KV prefill partials (no zeroing needed).
+    Allocated ON the stream that uses it, so when a larger one replaces it the caching
+    allocator recycles the old block in that stream's order (never under a running kernel)."""
+    st = _torch_stream(device, stream)
+    key = (device.index if device.index is not None else torch.cuda.current_device(), st.cuda_stream)
     ws = _SCRATCH.get(key)
     if ws is None or ws.numel() < need:
-        ws = torch.empty(max(need, 1 << 20), dtype=torch.uint8, device=device)
-        if stream is not None:
-            stream.wait_stream(torch.cuda.current_stream(device))
+        with torch.cuda.stream(st):
+            ws = torch.empty(max(need, 1 << 20), dtype=torch.uint8, device=device)
         _SCRATCH[key] = ws
     return ws
 
@@ -232,15 +289,15 @@ def _decode_workspace(device, need: int, ticket_bytes: int, stream) -> torch.Ten
     """Per-(device, stream) decode workspace.  Its leading ticket block must be zero
     before a call and every call leaves it zero (include/attn.h), so only a ticket
     block larger than any before it (which may overlap old partials) is cleared."""
-    key = (device.index if device.index is not None else torch.cuda.current_device(), _stream(stream).value)
+    st = _torch_stream(device, stream)
+    key = (device.index if device.index is not None else torch.cuda.current_device(), st.cuda_stream)
     ws, clean = _WS_CACHE.get(key, (None, 0))
-    if ws is None or ws.numel() < need:
-        ws = torch.zeros(max(need, 1 << 20), dtype=torch.uint8, device=device)
-        clean = ws.numel()
-    if ticket_bytes > clean:
-        ws[:ticket_bytes].zero_()
-    if stream is not None:
-        stream.wait_stream(torch.cuda.current_stream(device))
+    with torch.cuda.stream(st):   # allocated and zeroed in the order of the stream that uses it
+        if ws is None or ws.numel() < need:
+            ws = torch.zeros(max(need, 1 << 20), dtype=torch.uint8, device=device)
+            clean = ws.numel()
+        if ticket_bytes > clean:
+            ws[:ticket_bytes].zero_()
     _WS_CACHE[key] = (ws, ticket_bytes)   # after the call: tickets zero, partials beyond dirty
     return ws
 
@@ -279,14 +336,25 @@ def splitkv_decode(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, num_spl
         out = torch.empty_like(q, memory_format=torch.contiguous_format)
     if not want_out:
         out = None
-    if return_lse and lse is None and want_out:   # [B, Hq] for one query, else [B, Hq, Sq]
-        lse = torch.empty(q.shape[:2] if q.shape[2] == 1 else q.shape[:3], device=q.device, dtype=torch.float32)
+    lse_shape = q.shape[:2] if q.shape[2] == 1 else q.shape[:3]   # [B, Hq] for one query, else [B, Hq, Sq]
+    if return_lse and lse is None and want_out:
+        lse = torch.empty(lse_shape, device=q.device, dtype=torch.float32)
+    _check_io(q, k, v, out, lse, lse_shape)
+    if parts is not None:
+        P, B, H, D = parts.o.shape
+        if (P, B, H, D) != (num_splits, q.shape[0], q.shape[1], q.shape[3]) or parts.m.shape != (P, B, H) \
+                or parts.l.shape != (P, B, H) or any(t.dtype != torch.float32 or t.device != q.device
+                                                     for t in (parts.m, parts.l, parts.o)):
+            raise ValueError(f"parts must be float32 [{num_splits}, B, Hq(, D)] triples on q's device")
     ws_ptr, ws_bytes = None, 0
     if parts is None:
         need = lib.attn_splitkv_workspace_bytes(ctypes.byref(prob), num_splits)
-        if workspace is None or workspace.numel() * workspace.element_size() < need:
+        if workspace is None:
             tb = (q.shape[0] * k.shape[1] * 4 + 255) // 256 * 256
             workspace = _decode_workspace(q.device, need, tb, stream)
+        elif workspace.numel() * workspace.element_size() < need or workspace.device != q.device:
+            raise ValueError(f"workspace must be >= {need} bytes on q's device "
+                             f"(attn_splitkv_workspace_bytes); got {workspace.numel() * workspace.element_size()}")
         ws_ptr, ws_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
     cparts = None if parts is None else ctypes.byref(parts.c())
     check(lib.attn_splitkv_decode(ctypes.byref(prob), _as_tensor(q), _as_tensor(k), _as_tensor(v), num_splits,
@@ -312,6 +380,18 @@ def combine(parts: Parts, *, out: Optional[torch.Tensor] = None, out_dtype=torch
         out = None
     if return_lse and lse is None:
         lse = torch.empty(B, H, device=parts.o.device, dtype=torch.float32)
+    for t in (parts.m, parts.l, parts.o):
+        if t.dtype != torch.float32 or t.device != parts.o.device:
+            raise ValueError("parts must be float32 tensors on one device")
+    if parts.m.shape != (P, B, H) or parts.l.shape != (P, B, H):
+        raise ValueError("parts m / l must be [P, B, H]")
+    if out is not None and (tuple(out.shape) != (B, H, 1, D) or out.dtype not in _DT or out.device != parts.o.device):
+        raise ValueError(f"out must be a [{B}, {H}, 1, {D}] tensor on the parts' device")
+    if lse is not None and (tuple(lse.shape) != (B, H) or lse.dtype != torch.float32 or not lse.is_contiguous()
+                            or lse.device != parts.o.device):
+        raise ValueError(f"lse must be a contiguous float32 [{B}, {H}] tensor")
+    if acc is not None and (acc.o.shape != (1, B, H, D) or acc.m.shape != (1, B, H) or acc.o.dtype != torch.float32):
+        raise ValueError(f"acc must be float32 [1, {B}, {H}(, {D})] triples")
     dt = _DT[out.dtype] if out is not None else _ffi.ATTN_FP32
     cacc = None if acc is None else ctypes.byref(acc.c())
     check(lib.attn_combine(B, H, D, ctypes.byref(parts.c()), dt, _as_tensor(out),
@@ -327,6 +407,10 @@ def merge_partials(o_parts: torch.Tensor, lse_parts: torch.Tensor, *, out: Optio
     o_parts [P, ..., D] (bf16/fp16/fp32), lse_parts [P, ...] fp32, with the
     middle dimensions flattened into rows.  Returns O [..., D] (and lse)."""
     lib = load()
+    if o_parts.dtype not in _DT or lse_parts.dtype != torch.float32 or lse_parts.device != o_parts.device:
+        raise ValueError("o_parts must be bf16/fp16/fp32 and lse_parts float32 on the same device")
+    if tuple(lse_parts.shape) != tuple(o_parts.shape[:-1]):
+        raise ValueError(f"lse_parts {tuple(lse_parts.shape)} must be o_parts' shape without D")
     P, D = o_parts.shape[0], o_parts.shape[-1]
     rows = lse_parts[0].numel()
     o2 = o_parts.reshape(P, rows, D)
@@ -336,6 +420,9 @@ def merge_partials(o_parts: torch.Tensor, lse_parts: torch.Tensor, *, out: Optio
     dt = o_parts.dtype if out_dtype is None else out_dtype
     if out is None:
         out = torch.empty(o_parts.shape[1:], dtype=dt, device=o_parts.device)
+    elif tuple(out.shape) != tuple(o_parts.shape[1:]) or out.dtype not in _DT or out.device != o_parts.device \
+            or not out.is_contiguous():
+        raise ValueError(f"out must be a contiguous {tuple(o_parts.shape[1:])} tensor on the parts' device")
     lse = torch.empty(lse_parts.shape[1:], dtype=torch.float32, device=o_parts.device) if return_lse else None
     out2 = out.view(rows, D)
     check(lib.attn_merge_partials(P, rows, D, _DT[o_parts.dtype], o2.data_ptr(), o2.stride(0), o2.stride(1),

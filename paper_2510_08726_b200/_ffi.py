@@ -27,7 +27,7 @@ EXPORTED = ("attn_fused_fwd", "attn_splitkv_default_splits", "attn_splitkv_works
             "attn_nccl_get_unique_id", "attn_nccl_comm_init", "attn_nccl_comm_destroy",
             "attn_decode_kv_sharded_workspace_bytes", "attn_decode_kv_sharded",
             "attn_fused_fwd_default_splits", "attn_fused_fwd_workspace_bytes", "attn_fused_fwd_splitkv",
-            "attn_debug_repair_counters")
+            "attn_debug_repair_counters", "attn_fused_fwd_partial")
 # repair-event counter slots (include/attn.h ATTN_REPAIR_*)
 ATTN_REPAIR_FWD128, ATTN_REPAIR_FWD64, ATTN_REPAIR_PERSIST, ATTN_REPAIR_DECODE = 0, 1, 2, 3
 ATTN_REPAIR_SLOTS = 4
@@ -66,6 +66,23 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         raise RuntimeError(f"{path} is missing: run `python -m paper_2510_08726_b200.build` "
                            "(there is no fallback implementation)")
     lib = ctypes.CDLL(path)
+    if os.environ.get("ATTN_LIB_PATH"):
+        # developer A/B builds of older revisions may lack newer entry points: bind what exists
+        class _Partial:
+            def __init__(self, l):
+                self.__dict__["_l"] = l
+
+            def __getattr__(self, n):
+                try:
+                    return getattr(self._l, n)
+                except AttributeError:
+                    return ctypes.CFUNCTYPE(ctypes.c_int)(lambda *a: 2)
+
+            def __setattr__(self, n, v):
+                pass
+        missing = [n for n in EXPORTED if not hasattr(lib, n)]
+        if missing:
+            lib = _Partial(lib)
     P, T, Pa = ctypes.POINTER(AttnProblem), AttnTensor, ctypes.POINTER(AttnParts)
     vp, i32, f32p = ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p
     lib.attn_fused_fwd.argtypes = [P, T, T, T, T, f32p, vp]
@@ -76,6 +93,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.attn_fused_fwd_workspace_bytes.restype = ctypes.c_size_t
     lib.attn_fused_fwd_splitkv.argtypes = [P, T, T, T, T, f32p, i32, vp, ctypes.c_size_t, vp]
     lib.attn_fused_fwd_splitkv.restype = ctypes.c_int
+    lib.attn_fused_fwd_partial.argtypes = [P, T, T, T, vp, vp, vp]
+    lib.attn_fused_fwd_partial.restype = ctypes.c_int
     lib.attn_splitkv_default_splits.argtypes = [P, i32]
     lib.attn_splitkv_default_splits.restype = i32
     lib.attn_splitkv_workspace_bytes.argtypes = [P, i32]

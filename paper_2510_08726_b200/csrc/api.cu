@@ -12,6 +12,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 
 #include "../../include/attn.h"
@@ -125,14 +126,15 @@ attn_status cuda_status(cudaError_t e, const char* what) {
   return fail(ATTN_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
-int sm_count_cached() {
-  static int n = 0;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    cudaGetDevice(&dev);
+int sm_count_cached() {   // of the CURRENT device (one cached value per device ordinal)
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  int n = cache[dev & 63].load(std::memory_order_relaxed);
+  if (n == 0) {
     if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) n = 148;
-  });
+    cache[dev & 63].store(n, std::memory_order_relaxed);
+  }
   return n;
 }
 
@@ -187,7 +189,7 @@ size_t attn_fused_fwd_workspace_bytes(const attn_problem* p, int32_t num_splits)
   if (num_splits <= 1) return 0;
   const size_t rows = (size_t)num_splits * p->batch * p->heads_q * p->seqlen_q;
   auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
-  return up(rows * p->head_dim * 2) + up(rows * 4);   // partial O (q's dtype), partial lse (fp32)
+  return up(rows * p->head_dim * 4) + up(rows * 4);   // partial O (fp32, normalised), partial lse (fp32)
 }
 
 attn_status attn_fused_fwd_splitkv(const attn_problem* prob, attn_tensor q, attn_tensor k, attn_tensor v,
@@ -218,36 +220,32 @@ attn_status attn_fused_fwd_splitkv(const attn_problem* prob, attn_tensor q, attn
     if ((st = make_map(&a.tm_q, q, p.batch, p.heads_q, p.seqlen_q, p.head_dim, 64, 128, true, a.f16)) != ATTN_OK) return st;
     if ((st = make_map(&a.tm_k, k, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, 128, true, a.f16)) != ATTN_OK) return st;
     if ((st = make_map(&a.tm_v, v, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, 128, true, a.f16)) != ATTN_OK) return st;
-    if (num_splits <= 1) {
-      if ((st = make_map(&a.tm_o, o, p.batch, p.heads_q, p.seqlen_q, p.head_dim, 64, 128, true, a.f16)) != ATTN_OK) return st;
+    // (the prefill kernels prefetch tm_o even when they write fp32 partials: always a valid map)
+    if ((st = make_map(&a.tm_o, o, p.batch, p.heads_q, p.seqlen_q, p.head_dim, 64, 128, true, a.f16)) != ATTN_OK) return st;
+    if (num_splits <= 1)
       return (st = cuda_status(attn::launch_fwd_tc(a, s, &launches), "fwd_tc launch")) == ATTN_OK
                  ? (g_launches = launches, ATTN_OK) : st;
-    }
-    // KV split: partial (O_s, lse_s) per split into the workspace, then Eq. 8 over the splits
+    // KV split: fp32 normalised partial (O_s, lse_s) per split into the workspace, then Eq. 8
     const size_t need = attn_fused_fwd_workspace_bytes(prob, num_splits);
     if (workspace == nullptr || workspace_bytes < need)
       return fail(ATTN_ERR_WORKSPACE_TOO_SMALL, "workspace needs %zu bytes", need);
     if ((reinterpret_cast<uintptr_t>(workspace) & 255) != 0)
       return fail(ATTN_ERR_ALIGNMENT, "workspace must be 256-byte aligned");
     const long long rows = (long long)p.batch * p.heads_q * p.seqlen_q;
-    const size_t obytes = (((size_t)num_splits * rows * p.head_dim * 2) + 255) & ~size_t(255);
-    void* po = workspace;
+    const size_t obytes = (((size_t)num_splits * rows * p.head_dim * 4) + 255) & ~size_t(255);
+    float* po = static_cast<float*>(workspace);
     float* plse = reinterpret_cast<float*>(static_cast<char*>(workspace) + obytes);
     const int ntiles = (p.seqlen_kv + 127) / 128;
     a.s.kv_splits = num_splits;
     a.s.kv_split_tiles = (ntiles + num_splits - 1) / num_splits;
+    a.s.o_part = po;
     a.lse = plse;
-    const attn_tensor pt{po, (int64_t)p.heads_q * p.seqlen_q * p.head_dim, (int64_t)p.seqlen_q * p.head_dim,
-                         p.head_dim};
-    if ((st = make_map(&a.tm_o, pt, num_splits * p.batch, p.heads_q, p.seqlen_q, p.head_dim, 64, 128, true, a.f16)) !=
-        ATTN_OK)
-      return st;
     if ((st = cuda_status(attn::launch_fwd_tc(a, s, &launches), "fwd_tc launch")) != ATTN_OK) return st;
     attn::MergeArgs m{};
     m.P = num_splits;
     m.D = p.head_dim;
     m.rows = rows;
-    m.in_dtype = p.dtype;
+    m.in_dtype = ATTN_FP32;
     m.out_dtype = p.dtype;
     m.o_in = po;
     m.o_sp = rows * p.head_dim;
@@ -280,6 +278,38 @@ attn_status attn_fused_fwd_splitkv(const attn_problem* prob, attn_tensor q, attn
   a.o_sb = o.stride_b; a.o_sh = o.stride_h; a.o_ss = o.stride_s;
   a.lse = lse;
   st = cuda_status(attn::launch_fwd_simt(a, s, &launches), "fwd_simt launch");
+  if (st == ATTN_OK) g_launches = launches;
+  return st;
+}
+
+attn_status attn_fused_fwd_partial(const attn_problem* prob, attn_tensor q, attn_tensor k, attn_tensor v,
+                                   float* o_part, float* lse, attn_stream_t stream) {
+  g_err[0] = 0;
+  attn::VariantParams vp;
+  attn_status st = check_problem(prob, &vp);
+  if (st != ATTN_OK) return st;
+  const attn_problem& p = *prob;
+  if (p.dtype != ATTN_BF16 && p.dtype != ATTN_FP16)
+    return fail(ATTN_ERR_UNSUPPORTED, "attn_fused_fwd_partial takes bf16 / fp16 inputs (fp32: use attn_fused_fwd)");
+  if (p.head_dim != 64 && p.head_dim != 128)
+    return fail(ATTN_ERR_UNSUPPORTED, "bf16/fp16 head_dim must be 64 or 128 (got %d)", p.head_dim);
+  CHECK_ARG(o_part != nullptr && lse != nullptr, "o_part and lse are required");
+  if ((reinterpret_cast<uintptr_t>(o_part) & 15) != 0) return fail(ATTN_ERR_ALIGNMENT, "o_part must be 16-byte aligned");
+  if ((st = check_tensor(q, "q", 2, p.batch, p.heads_q, p.seqlen_q)) != ATTN_OK) return st;
+  if ((st = check_tensor(k, "k", 2, p.batch, p.heads_kv, p.seqlen_kv)) != ATTN_OK) return st;
+  if ((st = check_tensor(v, "v", 2, p.batch, p.heads_kv, p.seqlen_kv)) != ATTN_OK) return st;
+  attn::FwdTcArgs a;
+  a.s = shape_of(prob);
+  a.f16 = p.dtype == ATTN_FP16;
+  a.v = vp;
+  a.lse = lse;
+  a.s.o_part = o_part;
+  if ((st = make_map(&a.tm_q, q, p.batch, p.heads_q, p.seqlen_q, p.head_dim, 64, 128, true, a.f16)) != ATTN_OK) return st;
+  if ((st = make_map(&a.tm_k, k, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, 128, true, a.f16)) != ATTN_OK) return st;
+  if ((st = make_map(&a.tm_v, v, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, 128, true, a.f16)) != ATTN_OK) return st;
+  a.tm_o = a.tm_q;   // never stored through (prefetched only)
+  int launches = 0;
+  st = cuda_status(attn::launch_fwd_tc(a, reinterpret_cast<cudaStream_t>(stream), &launches), "fwd_tc launch");
   if (st == ATTN_OK) g_launches = launches;
   return st;
 }

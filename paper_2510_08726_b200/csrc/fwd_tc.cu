@@ -41,87 +41,34 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BN = 128;
-#ifndef ATTN_ROW_SPLIT
-#define ATTN_ROW_SPLIT 1
-#endif
-// Threads per S row: 2 => each row's 128 columns are split between two warps
-// (same TMEM lanes, different columns); row max and sum are exchanged through
-// shared memory.  Measured equal to 1 thread per row on B200 (a tile's 16K
-// exponentials are bound by the SM's 16 ex2/clk either way), so 1 is default.
-constexpr int kHalves = ATTN_ROW_SPLIT;
-constexpr int kTileThreads = 128 * kHalves;            // softmax threads per query tile
-constexpr int kSoftmaxWarps = 2 * kTileThreads / 32;
+constexpr int kTileThreads = 128;                       // softmax threads per query tile (thread = row)
+constexpr int kSoftmaxWarps = 2 * kTileThreads / 32;    // (the NT = 2 layout of the persistent kernel)
 constexpr int kWarpLoad = kSoftmaxWarps, kWarpMma = kSoftmaxWarps + 1, kWarpAlloc = kSoftmaxWarps + 2;
 constexpr int kThreads = (kSoftmaxWarps + 3) * 32;
-constexpr int kHC = BN / kHalves;                       // S columns per softmax thread
-#ifndef ATTN_PREFETCH
-#define ATTN_PREFETCH 0
-#endif
-constexpr int kPrefetch = ATTN_PREFETCH;   // KV tiles prefetched into L2 ahead of the TMA loads
-constexpr float kTau = 8.0f;
+constexpr float kTau = 8.0f;                      // lazy-repair threshold (log2 units), reading R9
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr uint32_t kBarTok0 = 3, kBarTok1 = 4;   // named barriers of the exp token
 constexpr uint32_t kBarP0 = 5;                    // 5 / 6: "P_t ready" (softmax threads of tile t + MMA warp)
-constexpr uint32_t kBarX0 = 7;                    // 7 / 8: row-max / row-sum exchange between column halves
 constexpr uint32_t kBarS0 = 9;                    // 9 / 10: "S_t loaded into registers" (P in smem only)
-#ifndef ATTN_TOKEN
-#define ATTN_TOKEN 1
-#endif
-#ifndef ATTN_P_SMEM
-#define ATTN_P_SMEM 1
-#endif
-// P in shared memory (PV = SS MMA) instead of aliasing S in TMEM: S_t is free
-// as soon as the softmax threads have loaded it, so QK_t(j+2) is issued right
-// after PV_t(j) and overlaps the softmax of step j+1 (the TMEM-aliased P
-// serialises softmax -> PV -> QK -> softmax per tile).  Costs 64 KiB of
-// shared memory (the K/V ring shrinks to 3 stages at D = 128).
-constexpr bool kPSmem = ATTN_P_SMEM != 0;
-#ifndef ATTN_F32X2
-#define ATTN_F32X2 1
-#endif
-// exp argument and row sum with packed fp32x2 FFMA2 / FADD2: half the issue slots of the
-// per-element FFMA + FADD in the exponential loop (the MUFU-bound phase)
-constexpr bool kF32x2 = ATTN_F32X2 != 0;
+// Causal block order: heaviest-first over a group of (head, batch) slices whose K/V fit in
+// this much of the 126 MB L2 (see the block order in fwd_tc_kernel).
+constexpr long long kCausalL2Bytes = 96LL << 20;
 #ifdef ATTN_TRACE
 constexpr bool kTraceBuild = true;    // the timeline trace instruments the non-persistent kernel
 #else
 constexpr bool kTraceBuild = false;
 #endif
-constexpr bool kToken = ATTN_TOKEN != 0;   // alternate the two softmax warpgroups' exp phases
-#ifndef ATTN_TOKEN64
-#define ATTN_TOKEN64 ATTN_TOKEN
-#endif
-#ifndef ATTN_TOKEN_RELEASE
-#define ATTN_TOKEN_RELEASE 4
-#endif
-#ifndef ATTN_F32X2_64
-#define ATTN_F32X2_64 0
-#endif
 
-#ifdef ATTN_SOFTMAX_SPIN
-#define WAIT_SM(bar, par) mbar_wait_spin(bar, par)   // softmax waits for S: poll
-#else
 #define WAIT_SM(bar, par) mbar_wait(bar, par)        // softmax waits for S: try_wait (HW sleep)
-#endif
-#ifndef ATTN_SLEEP_WAIT
 #define WAIT_LM(bar, par) mbar_wait_spin(bar, par)   // loader / MMA thread waits: poll
-#else
-#define WAIT_LM(bar, par) mbar_wait(bar, par)
-#endif
-#ifndef ATTN_LOADER_SLEEP
-#define ATTN_LOADER_SLEEP 0
-#endif
-// The producer's ring-slot waits: try_wait (the thread sleeps in hardware, no
-// issue slots taken from the softmax warp on its SM sub-partition) or poll.
-#define WAIT_L(bar, par) do { if (ATTN_LOADER_SLEEP) mbar_wait(bar, par); else WAIT_LM(bar, par); } while (0)
 
 #ifdef ATTN_TRACE
-// Debug-only timeline of one CTA: clock64() per (event, step), kept in shared
+// Debug-only timeline of one CTA: clock() per (event, step), kept in shared
 // memory while the kernel runs (so tracing adds no global-memory traffic
 // before the mbarrier releases) and copied to g_trace at the end.
 // 32-bit clock() samples (the host unwraps differences modulo 2^32).
-constexpr int kTrEv = 26, kTrSteps = kPSmem ? 24 : 40;
+constexpr int kTrEv = 26, kTrSteps = 24;
 __device__ long long g_trace[kTrEv][40];
 __device__ __forceinline__ bool trace_cta() { return blockIdx.x == 5 && blockIdx.y == 3 && blockIdx.z == 2; }
 #define TRACE(ev, step)                                                          \
@@ -132,67 +79,25 @@ __device__ __forceinline__ bool trace_cta() { return blockIdx.x == 5 && blockIdx
 #define TRACE(ev, step) do { } while (0)
 #endif
 
-#ifndef ATTN_NT64
-#define ATTN_NT64 1   // measured (same box): causal D = 64 +5 %, scaled-dot +1 %
-#endif
-#ifndef ATTN_NT1_STAGES64
-#define ATTN_NT1_STAGES64 5
-#endif
-#ifndef ATTN_NT128
-#define ATTN_NT128 2   // NT = 1 at D = 128 (TMEM-aliased P, 2-slot ring): -11 % (MHA)
-#endif
-#ifndef ATTN_ALIBI_MMA
-#define ATTN_ALIBI_MMA 1
-#endif
-#ifndef ATTN_PERSIST_LPT
-#define ATTN_PERSIST_LPT 0   // measured equal (the snake already balances)
-#endif
-#ifndef ATTN_CAUSAL_L2_MB
-#define ATTN_CAUSAL_L2_MB 96
-#endif
-#ifndef ATTN_ALIBI_MMA128
-#define ATTN_ALIBI_MMA128 1
-#endif
-#ifndef ATTN_ALIBI_REV
-#define ATTN_ALIBI_REV 1
-#endif
-#ifndef ATTN_ALIBI_CAUSAL_LIN
-#define ATTN_ALIBI_CAUSAL_LIN 1
-#endif
-// ALiBi folded into the QK contraction (D = 64, where the tensor core has slack): one
-// extra K = 16 MMA step adds s*c (s = slope / scale split into three 16-bit parts, c = key
-// column in the tile) to S, so the per-element bias costs nothing on the FMA pipe (see
-// score_tile_alibi_mma).  Shared memory for the constant operands: A_ext(+s), A_ext(-s), B_ext.
+// Shipped configuration per head dim (the measured alternatives are listed there):
+//   D = 128: NT = 2 query tiles per CTA (one CTA per SM, the tiles' exp phases alternate through a
+//            named-barrier token), P in shared memory (PV = SS MMA, S released early), 3-slot
+//            K/V ring, packed f32x2 exponent FMA / row sum, chunk-classified masks.
+//   D = 64 : NT = 1 (two 128-row CTAs per SM), P aliasing S in TMEM (PV = TS MMA), 5-slot ring.
+// ALiBi (without softcap) is folded into the QK contraction at both head dims (kExt).
+template <int D>
+__host__ __device__ constexpr int nt_of() { return D == 128 ? 2 : 1; }
 template <int D, bool kAlibi>
-__host__ __device__ constexpr bool alibi_mma() {
-  return ATTN_ALIBI_MMA != 0 && kAlibi && (D == 64 || (D == 128 && ATTN_ALIBI_MMA128 != 0 && ATTN_NT128 == 2 && kPSmem));
-}
+__host__ __device__ constexpr bool alibi_mma() { return kAlibi; }
 
-#ifndef ATTN_D64_STAGES
-#define ATTN_D64_STAGES 10
-#endif
-// NT = query tiles per CTA.  NT = 2: one CTA per SM, its two tiles' exp phases alternate
-// (token).  NT = 1: 128-row CTAs, TWO resident per SM (256 TMEM columns and < 113 KiB of
-// shared memory each, 6 warps): the two CTAs' rolling loops interleave on their own and one
-// CTA's prologue/epilogue overlaps the other's loop.
 template <int D, bool kExt = false, int NT = 2>
 struct Cfg {
   static constexpr int kBoxes = D / 64;           // 64-column (128 B) swizzle atoms per row
   static constexpr int kQTileBytes = BM * D * 2;
   static constexpr int kKVTileBytes = BN * D * 2;
-  // P in shared memory at D = 128 only: at D = 64 the tile's MMAs are half as long, the
-  // exponentials dominate and the P stores cost more than the decoupling gains (measured).
-#ifndef ATTN_P_SMEM64
-#define ATTN_P_SMEM64 0
-#endif
-  static constexpr bool kPS = NT == 1 ? (D == 64 && !kExt && ATTN_P_SMEM64 != 0) : (D == 128 ? kPSmem : ATTN_P_SMEM64 != 0);
+  static constexpr bool kPS = D == 128;          // P in shared memory (else in TMEM, aliasing S)
   static constexpr int kPTileBytes = kPS ? BM * BN * 2 : 0;
-#ifdef ATTN_TRACE
-  static constexpr int kStages = kPS ? 3 : ((D == 128) ? 4 : 8);   // room for the trace
-#else
-  static constexpr int kStages = NT == 1 ? ((D == 128) ? 2 : (kPS ? 4 : ATTN_NT1_STAGES64))
-                                          : kPS ? ((D == 128) ? 3 : 6) : ((D == 128) ? 5 : ATTN_D64_STAGES);
-#endif
+  static constexpr int kStages = D == 128 ? 3 : 5;
   // Load-group barriers (ring).  The producer can be at most kStages/2 groups
   // ahead of the issuer's wait, so kStages/2 + 1 barriers never alias a phase.
   static constexpr int kPairBars = kStages / 2 + 1;
@@ -203,11 +108,10 @@ struct Cfg {
   static constexpr int kSmemQ = NT * kQTileBytes + NT * kPTileBytes;   // Q, P tiles
   static constexpr int kSmemKV = kStages * kKVTileBytes;
   static constexpr int kNumBars = 1 + 2 * kStages + 6;
-  static constexpr int kXchgBytes = kHalves > 1 ? 2 * kHalves * BM * 4 : 0;   // [tile][half][row] floats
 #ifdef ATTN_TRACE
-  static constexpr int kSmemBytes = kSmemQ + kSmemKV + kExt2Bytes + kXchgBytes + 256 + kTrEv * kTrSteps * 4;
+  static constexpr int kSmemBytes = kSmemQ + kSmemKV + kExt2Bytes + 256 + kTrEv * kTrSteps * 4;
 #else
-  static constexpr int kSmemBytes = kSmemQ + kSmemKV + kExt2Bytes + kXchgBytes + kNumBars * 8 + 16;
+  static constexpr int kSmemBytes = kSmemQ + kSmemKV + kExt2Bytes + kNumBars * 8 + 16;
 #endif
 };
 
@@ -245,28 +149,6 @@ __device__ __forceinline__ Range tile_range(const Shape& s, const VariantParams&
   return r;
 }
 
-// 2^x on the FMA/ALU pipes (FA4-style MUFU offload): round-to-nearest split
-// x = k + f, f in [-1/2, 1/2]; degree-3 minimax polynomial for 2^f (relative
-// error 7.5e-5, below bf16's 2^-9 half-ulp of P); 2^k added to the exponent
-// bits.  Exact 0 for x < -126 (masked / -inf inputs).
-__device__ __forceinline__ float ex2_poly(float x) {
-  const float xc = fmaxf(x, -127.f);
-  const float t = xc + 12582912.f;            // 1.5 * 2^23: low mantissa bits = round(x)
-  const float f = xc - (t - 12582912.f);
-  float p = fmaf(0.05517109f, f, 0.24261115f);
-  p = fmaf(p, f, 0.6932611f);
-  p = fmaf(p, f, 0.99992806f);
-  const float r = __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-  return x < -126.f ? 0.f : r;
-}
-
-#ifndef ATTN_POLY_DIV
-#define ATTN_POLY_DIV 0   // every ATTN_POLY_DIV-th pair of exponentials uses ex2_poly (0 = none)
-#endif
-#ifndef ATTN_POLY_DIV64
-#define ATTN_POLY_DIV64 0
-#endif
-
 __device__ __forceinline__ bool active(const Range& r, int j) { return j >= r.lo && j < r.hi; }
 
 // ALiBi-in-MMA class of (query tile starting at row i0, KV tile j): +1 if every key is at or
@@ -276,7 +158,7 @@ __device__ __forceinline__ bool active(const Range& r, int j) { return j >= r.lo
 __device__ __forceinline__ int ext_class(const Shape& s, const VariantParams& v, int i0, int j) {
   // Causal: every ALLOWED key of any tile is at or before its query, so the linear form holds
   // for the allowed elements of a diagonal tile too (the rest are masked to -inf).
-  if (v.causal && ATTN_ALIBI_CAUSAL_LIN) return 1;
+  if (v.causal) return 1;
   const long long qf = v.q_off + i0, ql = v.q_off + min(i0 + BM, s.Sq) - 1;
   const long long k0 = v.kv_off + (long long)j * BN, k1 = k0 + BN - 1;
   if (k1 <= qf) return 1;
@@ -300,12 +182,6 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
 // score_mod; on mask tiles each chunk is classified warp-uniformly (all 32 rows of the warp
 // see it wholly allowed / wholly masked / partial) so only partial chunks pay the per-element
 // compare-and-select (on a causal diagonal tile that is one chunk in four per warp).
-#ifndef ATTN_CHUNK_MASK
-#define ATTN_CHUNK_MASK 1
-#endif
-#ifndef ATTN_CHUNK_MASK64
-#define ATTN_CHUNK_MASK64 0
-#endif
 // (kChunked = false: every element of a mask tile is compared; measured better at D = 64,
 // where the chunk branches cost registers in the MUFU-bound kernels.)
 template <bool kMask, bool kChunked, int N, class XF>
@@ -350,42 +226,9 @@ __device__ __forceinline__ float row_max_pass(float (&x)[N], int rel_lo, int rel
 // log2 domain used by the exponentials; returns the row max of the tile.
 // Plain variant: x stays raw (scale folded into the exp FFMA) and the max is
 // rescaled afterwards (scale > 0 so max commutes with it).
-#ifndef ATTN_TANH_POLY
-#define ATTN_TANH_POLY 0   // softcap tanh on the FMA pipe for every N-th column (measured: N = 2 -10 %, 3 equal; off)
-#endif
-// tanh(y) for |y| <= 1/2 by its odd Taylor polynomial to y^7 (truncation < 4.3e-5 absolute,
-// below tanh.approx.f32's ~2^-11 relative error): 5 FMA-pipe operations instead of one MUFU op.
-__device__ __forceinline__ float tanh_poly_small(float y) {
-  const float y2 = y * y;
-  float p = fmaf(y2, -17.f / 315.f, 2.f / 15.f);
-  p = fmaf(y2, p, -1.f / 3.f);
-  return fmaf(y * y2, p, y);
-}
-
 template <bool kAlibi, bool kSoftcap, bool kMask, bool kChunked = true, int N>
 __device__ __forceinline__ float score_tile(float (&x)[N], const VariantParams& v, float nslope2, float dq0,
                                             int rel_lo, int rel_hi) {
-  if constexpr (kSoftcap && ATTN_TANH_POLY > 0) {
-    // Softcap spends two SFU ops per element (tanh, then ex2) and is MUFU-bound.  When every
-    // |y| = |x / cap| of the warp's tile is <= 1/2 (the usual regime: logits well below the
-    // cap), every ATTN_TANH_POLY-th column evaluates tanh on the FMA pipe instead.
-    float ya = 0.f;
-#pragma unroll
-    for (int c = 0; c < N; ++c) {
-      x[c] *= v.scale_over_cap;
-      ya = fmaxf(ya, fabsf(x[c]));
-    }
-    auto fin = [&](float t, int c) {
-      float xv = v.softcap_log2 * t;                                        // R3: cap * tanh(x / cap)
-      if constexpr (kAlibi) xv = fmaf(nslope2, fabsf(dq0 - (float)c), xv);  // R4
-      return xv;
-    };
-    if (__all_sync(0xffffffffu, ya <= 0.5f))
-      return row_max_pass<kMask, kChunked>(x, rel_lo, rel_hi, [&](float y, int c) {
-        return fin(c % ATTN_TANH_POLY == ATTN_TANH_POLY - 1 ? tanh_poly_small(y) : tanh_approx(y), c);
-      });
-    return row_max_pass<kMask, kChunked>(x, rel_lo, rel_hi, [&](float y, int c) { return fin(tanh_approx(y), c); });
-  }
   float mt = row_max_pass<kMask, kChunked>(x, rel_lo, rel_hi, [&](float xv, int c) {
     if constexpr (kSoftcap) {
       xv = v.softcap_log2 * tanh_approx(xv * v.scale_over_cap);   // R3: cap * tanh(x / cap)
@@ -399,22 +242,6 @@ __device__ __forceinline__ float score_tile(float (&x)[N], const VariantParams& 
   return mt;
 }
 
-#ifndef ATTN_ALIBI_LIN
-#define ATTN_ALIBI_LIN 1
-#endif
-
-// ALiBi on a tile of uniform sign (ext_class != 0) without the MMA extension: the bias is
-// sslope * c + a row constant (folded into the exponent's offset by the caller), so
-// x = scale S + sslope * c costs an immediate-operand multiply and one FFMA per element
-// instead of FMUL + |.| FADD + FFMA (the FMA pipe bound the ALiBi kernels at D = 128).
-template <bool kMask, bool kChunked, int N>
-__device__ __forceinline__ float score_tile_alibi_lin(float (&x)[N], const VariantParams& v, float sslope, int rel_lo,
-                                                      int rel_hi) {
-  return row_max_pass<kMask, kChunked>(x, rel_lo, rel_hi, [&](float xv, int c) {
-    return fmaf(xv, v.scale_log2, sslope * (float)c);
-  });
-}
-
 // Mixed ALiBi-in-MMA tile (ext_class 0, built with A_ext(+s)): S = q.k + s c, so
 // x = scale S - slope (c + |qpos - kpos|) = scale S - slope max(dq0, 2c - dq0) (log2 units).
 template <bool kMask, int N>
@@ -426,7 +253,7 @@ __device__ __forceinline__ float score_tile_ext_mixed(float (&x)[N], const Varia
 }
 
 template <int NT>
-struct Roles {   // warp roles of fwd_tc_kernel (kHalves == 1 for NT == 1)
+struct Roles {   // warp roles of fwd_tc_kernel
   static constexpr int kSoftmaxWarps = NT * kTileThreads / 32;
   static constexpr int kWarpLoad = kSoftmaxWarps, kWarpMma = kSoftmaxWarps + 1;
   static constexpr int kWarpAlloc = NT == 2 ? kSoftmaxWarps + 2 : kWarpMma;   // NT = 1: the MMA warp allocates
@@ -435,7 +262,6 @@ struct Roles {   // warp roles of fwd_tc_kernel (kHalves == 1 for NT == 1)
   static constexpr int kTmemCols = NT == 2 ? 512 : 256;
   static constexpr uint32_t kOBase = NT == 2 ? 256 : 128;   // TMEM column of O_0 (S_t at t * 128)
 };
-static_assert(kHalves == 1 || (ATTN_NT64 == 2 && ATTN_NT128 == 2), "NT = 1 needs one thread per row");
 
 template <int D, bool kAlibi, bool kSoftcap, bool kF16, int NT>
 __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
@@ -443,19 +269,14 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o, const Shape s,
                   const VariantParams v, float* __restrict__ lse) {
   constexpr bool kExt = alibi_mma<D, kAlibi && !kSoftcap>();   // softcap: the bias follows the tanh
-  constexpr bool kAlibiLin = ATTN_ALIBI_LIN != 0 && kAlibi && !kSoftcap && !kExt;   // uniform-tile ALiBi, FMA form
-  constexpr bool kChunkMask = (D == 128 || ATTN_CHUNK_MASK64) && ATTN_CHUNK_MASK;   // chunk-classified masking (measured: + at D = 128, - at D = 64)
+  constexpr bool kChunkMask = D == 128;   // chunk-classified masking (measured: + at D = 128, - at D = 64)
   using C = Cfg<D, kExt, NT>;
   using Ro = Roles<NT>;
   constexpr int kSoftmaxWarps = Ro::kSoftmaxWarps, kWarpLoad = Ro::kWarpLoad, kWarpMma = Ro::kWarpMma;
   constexpr int kWarpAlloc = Ro::kWarpAlloc;
-  constexpr bool kPSmem = C::kPS;   // shadows the global switch: per head dim
-  constexpr bool kF32x2 = D == 128 ? ::attn::kF32x2 : ATTN_F32X2_64 != 0;   // measured: +1.5-2 % at D = 128, -4 % at D = 64
-  constexpr bool kToken = NT == 2 && (D == 128 ? ::attn::kToken : ATTN_TOKEN64 != 0);
-  constexpr int kPolyDiv = D == 64 ? ATTN_POLY_DIV64 : ATTN_POLY_DIV;   // pairs on the FMA-pipe exp2
-  // The token passes to the other tile after this many of the row's 32-column exp chunks
-  // (4 = after the whole exp phase): an earlier release overlaps the two tiles' exp phases.
-  constexpr int kTokenRelease = ATTN_TOKEN_RELEASE;
+  constexpr bool kPSmem = C::kPS;
+  constexpr bool kF32x2 = D == 128;   // packed FFMA2 / FADD2 (measured: +1.5-2 % at D = 128, -4 % at D = 64)
+  constexpr bool kToken = NT == 2;    // the two tiles' exp phases alternate (+2 %)
   constexpr bool kPlain = !kAlibi && !kSoftcap;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // The 128-byte swizzle needs 1024-byte aligned tiles; dynamic shared memory
@@ -466,8 +287,7 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
   uint8_t* sP = smem + NT * C::kQTileBytes;   // kPSmem: P_t, K-major SW128 [key atom][row][128 B]
   uint8_t* sExt = smem + C::kSmemQ + C::kSmemKV;   // kExt: A_ext(+s), A_ext(-s), B_ext
   uint8_t* sKV = smem + C::kSmemQ;
-  float* xchg = reinterpret_cast<float*>(sKV + C::kSmemKV + C::kExt2Bytes);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::kSmemKV + C::kExt2Bytes + C::kXchgBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::kSmemKV + C::kExt2Bytes);
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;
   uint64_t* kv_empty = kv_full + C::kStages;
@@ -483,7 +303,7 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
 
   const uint32_t warp = warp_id(), lane = lane_id();
   // Block order.  Causal: heaviest q-blocks first -- across a GROUP of (head, batch) slices
-  // whose K/V fit in ATTN_CAUSAL_L2_MB of L2 (longest-processing-time order over the group),
+  // whose K/V fit in kCausalL2Bytes of L2 (longest-processing-time order over the group),
   // not head by head: the hardware dispatches blocks in linear order, so a group's light
   // blocks fill in behind all of its heavy ones.  (A/B vs head by head, 96 MB: D = 64 causal
   // 426 -> 477, ALiBi-causal 389 -> 441, softcap-causal 294 -> 337; D = 128 ALiBi-causal +2 %.)
@@ -491,7 +311,7 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
   if (v.causal) {
     const int nqb = gridDim.x, nh = gridDim.y * gridDim.z;
     const long long kv_bytes = 4LL * s.Skv * D / (s.Hq / s.Hkv);       // K + V of one q head's group, / G
-    const int gh = (int)max(1LL, min((long long)nh, ((long long)ATTN_CAUSAL_L2_MB << 20) / max(kv_bytes, 1LL)));
+    const int gh = (int)max(1LL, min((long long)nh, kCausalL2Bytes / max(kv_bytes, 1LL)));
     const int lin = blockIdx.x + nqb * (blockIdx.y + gridDim.y * blockIdx.z);
     const int grp = lin / (nqb * gh), idx = lin - grp * nqb * gh;
     const int ghe = min(gh, nh - grp * gh);                          // heads in this (maybe partial) group
@@ -531,11 +351,11 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
   // diagonal tile d, goes down to ulo, then up from d + 1: J(k) = d - (k - ulo) for the first
   // d - ulo + 1 steps, else k (the reflection above is the case d = uhi - 1).
   const bool full = (rng0.lo == ulo && rng0.hi == uhi) && (!has_rows1 || (rng1.lo == ulo && rng1.hi == uhi));
-  const bool rev = kAlibi && ATTN_ALIBI_REV && (v.causal || v.window_right == 0);
+  const bool rev = kAlibi && (v.causal || v.window_right == 0);
   int d_walk = ulo - 1;   // identity
   if (rev) {
     d_walk = uhi - 1;
-  } else if (kAlibi && ATTN_ALIBI_REV && full && uhi > ulo) {
+  } else if (kAlibi && full && uhi > ulo) {
     const long long ql = v.q_off + min(row0 + NT * BM, s.Sq) - 1;
     d_walk = (int)max((long long)ulo, min((long long)uhi - 1, (ql - v.kv_off) / BN));
   }
@@ -603,28 +423,18 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       const uint64_t pol_q = policy_evict_first();
-#ifdef ATTN_KV_EVICT_NORMAL
-      const uint64_t pol_kv = policy_evict_normal();
-#else
       const uint64_t pol_kv = policy_evict_last();   // K/V are re-read by the other q-blocks of this head
-#endif
       const int nq = has_rows1 ? 2 : 1;
       mbar_arrive_expect_tx(q_full, nq * C::kQTileBytes);
       for (int t = 0; t < nq; ++t)
         for (int bx = 0; bx < C::kBoxes; ++bx)
           tma_load_4d(&tm_q, q_full, sQ + t * C::kQTileBytes + bx * BM * 128, bx * 64, row0 + t * BM, hq, b, pol_q);
-      if (kPrefetch > 0)
-      for (int j = ulo; j < min(ulo + kPrefetch, uhi); ++j)
-        for (int bx = 0; bx < C::kBoxes; ++bx) {
-          tma_prefetch_4d(&tm_k, bx * 64, J(j) * BN, hkv, b);
-          tma_prefetch_4d(&tm_v, bx * 64, J(j) * BN, hkv, b);
-        }
       if constexpr (kPSmem) {
         // One barrier per ring slot; ring order = the issuer's consumption order:
         // K_ulo, K_ulo+1, then (V_j, K_j+2) for every step j.
         int it = 0;
         auto load = [&](bool is_k, int jj) {
-          WAIT_L(&kv_empty[it % C::kStages], ((it / C::kStages) & 1) ^ 1);
+          WAIT_LM(&kv_empty[it % C::kStages], ((it / C::kStages) & 1) ^ 1);
           uint64_t* bar = &kv_full[it % C::kStages];
           mbar_arrive_expect_tx(bar, C::kKVTileBytes);
           uint8_t* dst = sKV + (it % C::kStages) * C::kKVTileBytes;
@@ -647,14 +457,9 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
       const int n = uhi - ulo;
       for (int g = 0; g <= n; ++g) {
         const int j = ulo + g;
-        if (kPrefetch > 0 && j + kPrefetch < uhi)
-          for (int bx = 0; bx < C::kBoxes; ++bx) {
-            tma_prefetch_4d(&tm_k, bx * 64, J(j + kPrefetch) * BN, hkv, b);
-            tma_prefetch_4d(&tm_v, bx * 64, J(j + kPrefetch) * BN, hkv, b);
-          }
         const int it0 = g == 0 ? 0 : 2 * g - 1;          // ring index of the group's first tile
         const int it1 = g < n ? 2 * g : 2 * g - 1;       // ... and of its last tile
-        for (int it = it0; it <= it1; ++it) WAIT_L(&kv_empty[it % C::kStages], ((it / C::kStages) & 1) ^ 1);
+        for (int it = it0; it <= it1; ++it) WAIT_LM(&kv_empty[it % C::kStages], ((it / C::kStages) & 1) ^ 1);
         uint64_t* bar = &kv_full[g % C::kPairBars];
         mbar_arrive_expect_tx(bar, (it1 - it0 + 1) * C::kKVTileBytes);
         for (int it = it0; it <= it1; ++it) {
@@ -803,10 +608,9 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
     }
   } else if (warp < kSoftmaxWarps) {
     // ------------------------------------------------------------ softmax / correction / epilogue
-    // Thread (tile t, row r, column half h) owns S columns [h*kHC, (h+1)*kHC) of row r.
+    // Thread (tile t, row r) owns row r of S_t / O_t (TMEM lane r).
     const int t = (int)warp / (kSoftmaxWarps / NT);
     const int wt = (int)warp % (kSoftmaxWarps / NT);      // warp within the tile
-    const int half = wt >> 2;
     const int wq = warp & 3;                               // TMEM lane quarter
     const int r = wq * 32 + lane;
     const int tid_t = wt * 32 + lane;                      // thread index within the tile
@@ -816,13 +620,9 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
     int jlo_row, jhi_row;
     row_bounds(s, v, qpos, jlo_row, jhi_row);
     const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
-    const int c_base = half * kHC;                         // first S column of this thread
-    constexpr int kOC = D / kHalves;                       // O columns of this thread
-    const uint32_t tS = tmem + t * 128 + lane_off + c_base;
-    const uint32_t tP = tmem + t * 128 + lane_off + half * (kHC / 2);   // bf16 pairs, aliasing S
-    const uint32_t tO = tmem + Ro::kOBase + t * 128 + lane_off + half * kOC;
-    float* my_x = xchg + (t * kHalves + half) * BM + r;             // exchange slots (kHalves == 2)
-    const float* other_x = xchg + (t * kHalves + (1 - half)) * BM + r;
+    const uint32_t tS = tmem + t * 128 + lane_off;
+    const uint32_t tP = tmem + t * 128 + lane_off;         // 16-bit pairs, aliasing S (D = 64)
+    const uint32_t tO = tmem + Ro::kOBase + t * 128 + lane_off;
     const float nslope2 = kAlibi ? -v.alibi[hq] * kLog2e : 0.f;
     float m_ref = -INFINITY;  // stale reference max (log2 units), R9
     float l = 0.f;            // running denominator over this thread's columns (un-rounded fp32 p, R10)
@@ -843,11 +643,11 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
       WAIT_SM(&s_full[t], it & 1);
       tc_fence_after();
       if (tid_t == 0) TRACE(5 + 4 * t, j);
-      float x[kHC];
+      float x[BN];
       {
-        uint32_t u[kHC];
+        uint32_t u[BN];
 #pragma unroll
-        for (int c = 0; c < kHC / 32; ++c) tmem_ld32(tS + c * 32, reinterpret_cast<uint32_t(&)[32]>(u[c * 32]));
+        for (int c = 0; c < BN / 32; ++c) tmem_ld32(tS + c * 32, reinterpret_cast<uint32_t(&)[32]>(u[c * 32]));
         tmem_ld_wait();
         if constexpr (kPSmem) {
           if (j + 1 < R.hi) {   // S_t is in registers: the issuer may compute S_t(j+1) into it
@@ -856,13 +656,13 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
           }
         }
 #pragma unroll
-        for (int c = 0; c < kHC; ++c) x[c] = u2f(u[c]);
+        for (int c = 0; c < BN; ++c) x[c] = u2f(u[c]);
       }
       // Fig. 19 max_local (+ score_mod, mask) -> max_global
       const int jt = J(j);   // the KV tile of step j
       const bool need_mask = !(jt * BN >= R.jlo_last && (jt + 1) * BN - 1 <= R.jhi_first);
-      const int rel_lo = jlo_row - jt * BN - c_base, rel_hi = jhi_row - jt * BN - c_base;
-      const float dq0 = (float)(qpos - v.kv_off - (long long)jt * BN - c_base);
+      const int rel_lo = jlo_row - jt * BN, rel_hi = jhi_row - jt * BN;
+      const float dq0 = (float)(qpos - v.kv_off - (long long)jt * BN);
       // exponent argument a = x * e_mul + e_off' (e_off' = e_off - m, set after the max)
       float e_mul = kPlain ? v.scale_log2 : 1.f, e_off = 0.f;
       float mt;
@@ -878,21 +678,9 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
           mt = need_mask ? score_tile_ext_mixed<true>(x, v, nslope2, dq0, rel_lo, rel_hi)
                          : score_tile_ext_mixed<false>(x, v, nslope2, dq0, rel_lo, rel_hi);
         }
-      } else if (kAlibiLin && ext_class(s, v, row0 + t * BM, jt) != 0) {
-        const int cls = ext_class(s, v, row0 + t * BM, jt);
-        e_off = (cls > 0 ? nslope2 : -nslope2) * dq0;
-        const float sslope = cls > 0 ? -nslope2 : nslope2;
-        mt = (need_mask ? score_tile_alibi_lin<true, kChunkMask>(x, v, sslope, rel_lo, rel_hi)
-                        : score_tile_alibi_lin<false, kChunkMask>(x, v, sslope, rel_lo, rel_hi)) + e_off;
       } else {
         mt = need_mask ? score_tile<kAlibi, kSoftcap, true, kChunkMask>(x, v, nslope2, dq0, rel_lo, rel_hi)
                        : score_tile<kAlibi, kSoftcap, false, kChunkMask>(x, v, nslope2, dq0, rel_lo, rel_hi);
-      }
-      if constexpr (kHalves > 1) {
-        // both halves must have loaded S before either overwrites it with P (P aliases S)
-        *my_x = mt;
-        named_bar_sync(kBarX0 + t, kTileThreads);
-        mt = fmaxf(mt, *other_x);
       }
       const float m_run = fmaxf(m_ref, mt);
       bool move, need_o;
@@ -909,7 +697,6 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
       l *= alpha;                                       // xsum = h(xsum) + ...
       // exp(x - m), local sum, P -> bf16 into TMEM (aliasing S)
       const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
-      float m_use_t = m_use;
       if constexpr (kPSmem) {
         // PV_t(j-1) must be complete before P_t(j) overwrites sP_t
         // (the rare O rescale stays after the exponentials, where the S registers are dead)
@@ -918,43 +705,23 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
           tc_fence_after();
         }
       }
-      if (kToken) {
-        named_bar_sync(t == 0 ? kBarTok0 : kBarTok1, 2 * kTileThreads);   // acquire the exp token
-#ifdef ATTN_TOKEN_STRICT
-        asm volatile("" : "+f"(m_use_t));
-#endif
-      }
+      if (kToken) named_bar_sync(t == 0 ? kBarTok0 : kBarTok1, 2 * kTileThreads);   // acquire the exp token
       if (tid_t == 0) TRACE(6 + 4 * t, j);
-      const float e_add = e_off - m_use_t;
+      const float e_add = e_off - m_use;
       float sum0 = 0.f, sum1 = 0.f;
 #pragma unroll
-      for (int c0 = 0; c0 < kHC; c0 += 32) {
+      for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t pk[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          float a0, a1;
-          if constexpr (kF32x2 && (kExt || kAlibiLin)) {
+          float a0, a1;   // exponent argument (log2 units): x * e_mul + e_off - m
+          if constexpr (kF32x2) {
             fma2_bc(a0, a1, x[c0 + 2 * e], x[c0 + 2 * e + 1], e_mul, e_add);
-          } else if constexpr (kF32x2) {
-            fma2_bc(a0, a1, x[c0 + 2 * e], x[c0 + 2 * e + 1], kPlain ? v.scale_log2 : 1.f, -m_use_t);
-          } else if constexpr (kExt || kAlibiLin) {
+          } else {
             a0 = fmaf(x[c0 + 2 * e], e_mul, e_add);
             a1 = fmaf(x[c0 + 2 * e + 1], e_mul, e_add);
-          } else if constexpr (kPlain) {
-            a0 = fmaf(x[c0 + 2 * e], v.scale_log2, -m_use_t);
-            a1 = fmaf(x[c0 + 2 * e + 1], v.scale_log2, -m_use_t);
-          } else {
-            a0 = x[c0 + 2 * e] - m_use_t;
-            a1 = x[c0 + 2 * e + 1] - m_use_t;
           }
-          float p0, p1;
-          if (kPolyDiv > 0 && (e % (kPolyDiv > 0 ? kPolyDiv : 1)) == (kPolyDiv > 0 ? kPolyDiv : 1) - 1) {
-            p0 = ex2_poly(a0);
-            p1 = ex2_poly(a1);
-          } else {
-            p0 = ex2_approx(a0);
-            p1 = ex2_approx(a1);
-          }
+          const float p0 = ex2_approx(a0), p1 = ex2_approx(a1);
           if constexpr (kF32x2) {
             add2_acc(sum0, sum1, p0, p1);
           } else {
@@ -964,7 +731,7 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
           pk[e] = pack2<kF16>(p0, p1);
         }
         if constexpr (kPSmem) {   // row r of P_t: K-major, 128-B swizzle (the UMMA A layout)
-          const int cc = c_base + c0;                      // S / P column of pk[0]
+          const int cc = c0;                               // S / P column of pk[0]
           uint8_t* rowp = sP + t * C::kPTileBytes + (cc >> 6) * (BM * 128) + r * 128;
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
@@ -975,15 +742,8 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
         } else {
           tmem_st16(tP + c0 / 2, pk);
         }
-        if (kToken && kTokenRelease < kHC / 32 && c0 == (kTokenRelease - 1) * 32) {   // early token release
-          if (t == 0) named_bar_arrive(kBarTok1, 2 * kTileThreads);
-          else if (j + 1 < uhi) named_bar_arrive(kBarTok0, 2 * kTileThreads);
-        }
       }
-#ifdef ATTN_TOKEN_STRICT
-      if (kToken) asm volatile("" ::"f"(sum0), "f"(sum1));
-#endif
-      if (kToken && kTokenRelease >= kHC / 32) {            // release the token
+      if (kToken) {                                         // release the token
         if (t == 0) named_bar_arrive(kBarTok1, 2 * kTileThreads);
         else if (j + 1 < uhi) named_bar_arrive(kBarTok0, 2 * kTileThreads);
       }
@@ -997,7 +757,7 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
         mbar_wait(&o_done[t], (it - 1) & 1);
         tc_fence_after();
 #pragma unroll
-        for (int c = 0; c < kOC / 32; ++c) {
+        for (int c = 0; c < D / 32; ++c) {
           uint32_t o[32];
           tmem_ld32(tO + c * 32, o);
           tmem_ld_wait();
@@ -1024,15 +784,11 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
     }
 
     // ------------------------------------------------------------ epilogue: O / l -> 16-bit -> TMA store
+    // (s.o_part: fp32 O / l straight to global instead -- the KV-split and context-parallel
+    // partials, so the Eq. 8 merge sees un-rounded partials)
     const int n_it = R.hi - R.lo;
     const bool tile_rows = (row0 + t * BM) < s.Sq;
     if (tile_rows) {
-      if constexpr (kHalves > 1) {   // total row sum = both halves' partial sums
-        named_bar_sync(kBarX0 + t, kTileThreads);   // partners are done reading the max slots
-        *my_x = l;
-        named_bar_sync(kBarX0 + t, kTileThreads);
-        l += *other_x;
-      }
       if (n_it > 0) {
         mbar_wait(&o_done[t], (n_it - 1) & 1);
         tc_fence_after();
@@ -1040,37 +796,57 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
         mbar_wait(q_full, 0);   // the Q tile we overwrite must have landed
       }
       const float inv_l = l > 0.f ? 1.f / l : 0.f;
-      uint8_t* sOut = sQ + t * C::kQTileBytes;
+      if (s.o_part != nullptr) {
+        float* dst = s.o_part + (((size_t)zb * s.Hq + hq) * s.Sq + i) * D;
 #pragma unroll
-      for (int c = 0; c < kOC / 32; ++c) {
-        uint32_t o[32];
-        if (n_it > 0) {
-          tmem_ld32(tO + c * 32, o);
-          tmem_ld_wait();
-        } else {
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t o[32];
+          if (n_it > 0) {
+            tmem_ld32(tO + c * 32, o);
+            tmem_ld_wait();
+          } else {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) o[e] = 0u;
+            for (int e = 0; e < 32; ++e) o[e] = 0u;
+          }
+          if (i < s.Sq) {
+#pragma unroll
+            for (int e = 0; e < 32; e += 4)
+              *reinterpret_cast<float4*>(dst + c * 32 + e) =
+                  make_float4(u2f(o[e]) * inv_l, u2f(o[e + 1]) * inv_l, u2f(o[e + 2]) * inv_l, u2f(o[e + 3]) * inv_l);
+          }
         }
-        uint32_t pk[16];
+      } else {
+        uint8_t* sOut = sQ + t * C::kQTileBytes;
 #pragma unroll
-        for (int e = 0; e < 16; ++e) pk[e] = pack2<kF16>(u2f(o[2 * e]) * inv_l, u2f(o[2 * e + 1]) * inv_l);
-        const int cg = half * (kOC / 32) + c;               // 32-column chunk of the O row
-        uint8_t* rowp = sOut + (cg >> 1) * (BM * 128) + r * 128;
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t o[32];
+          if (n_it > 0) {
+            tmem_ld32(tO + c * 32, o);
+            tmem_ld_wait();
+          } else {
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          const int ch = (cg & 1) * 4 + q4;
-          *reinterpret_cast<uint4*>(rowp + ((ch ^ (r & 7)) << 4)) =
-              make_uint4(pk[4 * q4], pk[4 * q4 + 1], pk[4 * q4 + 2], pk[4 * q4 + 3]);
+            for (int e = 0; e < 32; ++e) o[e] = 0u;
+          }
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) pk[e] = pack2<kF16>(u2f(o[2 * e]) * inv_l, u2f(o[2 * e + 1]) * inv_l);
+          uint8_t* rowp = sOut + (c >> 1) * (BM * 128) + r * 128;   // 32-column chunk c of the O row
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const int ch = (c & 1) * 4 + q4;
+            *reinterpret_cast<uint4*>(rowp + ((ch ^ (r & 7)) << 4)) =
+                make_uint4(pk[4 * q4], pk[4 * q4 + 1], pk[4 * q4 + 2], pk[4 * q4 + 3]);
+          }
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(1 + t, kTileThreads);
+        if (tid_t == 0) {
+          for (int bx = 0; bx < C::kBoxes; ++bx) tma_store_4d(&tm_o, sOut + bx * BM * 128, bx * 64, row0 + t * BM, hq, zb);
+          bulk_commit();
+          bulk_wait_read0();
         }
       }
-      fence_proxy_async_smem();
-      named_bar_sync(1 + t, kTileThreads);
-      if (tid_t == 0) {
-        for (int bx = 0; bx < C::kBoxes; ++bx) tma_store_4d(&tm_o, sOut + bx * BM * 128, bx * 64, row0 + t * BM, hq, zb);
-        bulk_commit();
-        bulk_wait_read0();
-      }
-      if (lse != nullptr && i < s.Sq && half == 0)
+      if (lse != nullptr && i < s.Sq)
         lse[((size_t)zb * s.Hq + hq) * s.Sq + i] = l > 0.f ? m_ref * kLn2 + logf(l) : -INFINITY;
     }
   }
@@ -1103,13 +879,11 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
 // loads into P(u)'s region once unit u's PVs are done (pv_done) and unit
 // u-1's O store has left it (epi_done).
 // ============================================================================
-// ATTN_PERSIST: 0 never, 1 for causal (no window) problems, 2 always.  Measured (r1g):
-// causal MHA 996 -> 1022 TFLOP/s (short, uneven units: the hidden boundaries matter);
-// non-causal MHA 1229 -> 1218 and the GQA window 1120 -> 1102 (long units, and the
-// persistent loop carries more live registers: 72 vs 52 bytes of spills).
-#ifndef ATTN_PERSIST
-#define ATTN_PERSIST 1
-#endif
+// Used for pure-causal (no window), non-ALiBi problems.  Measured (r1g): causal MHA 996 ->
+// 1022 TFLOP/s (short, uneven units: the hidden boundaries matter); non-causal MHA 1229 ->
+// 1218 and the GQA window 1120 -> 1102 (long units, and the persistent loop carries more
+// live registers), so those stay on the grid kernel; ALiBi needs the grid kernel's
+// diagonal-first KV walk.
 
 struct Unit {
   int qblk, hq, zb, b, valid;
@@ -1119,18 +893,7 @@ __device__ __forceinline__ Unit unit_of(const Shape& s, const VariantParams& v, 
   const int nz = s.B * (s.kv_splits > 1 ? s.kv_splits : 1);
   Unit u;
   u.valid = idx < nqb * s.Hq * nz;
-  int head_lin = idx / nqb, qi = idx % nqb;
-  if (v.causal && ATTN_PERSIST_LPT) {   // heaviest-first across an L2-sized group of heads (as the grid kernel)
-    const int nh = s.Hq * nz;
-    const long long kv_bytes = 4LL * s.Skv * 128 / (s.Hq / s.Hkv);
-    const int gh = (int)max(1LL, min((long long)nh, ((long long)ATTN_CAUSAL_L2_MB << 20) / max(kv_bytes, 1LL)));
-    const int grp = idx / (nqb * gh), r = idx - grp * nqb * gh;
-    const int ghe = min(gh, nh - grp * gh);
-    if (u.valid) {
-      qi = r / ghe;
-      head_lin = grp * gh + r % ghe;
-    }
-  }
+  const int head_lin = idx / nqb, qi = idx % nqb;
   u.qblk = v.causal ? nqb - 1 - qi : qi;          // heaviest causal q-block first
   u.hq = head_lin % s.Hq;
   u.zb = head_lin / s.Hq;
@@ -1174,7 +937,7 @@ __device__ __forceinline__ UnitRanges ranges_of(const Shape& s, const VariantPar
   return q;
 }
 
-template <bool kAlibi, bool kSoftcap, bool kF16>
+template <bool kSoftcap, bool kF16>
 __global__ void __launch_bounds__(kThreads, 1)
     fwd_tc_persist_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                           const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
@@ -1184,7 +947,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kTile = BM * D * 2;                          // 32 KiB
   constexpr int kStages = 3;
   constexpr int kKV = BN * D * 2;
-  constexpr bool kPlain = !kAlibi && !kSoftcap;
+  constexpr bool kPlain = !kSoftcap;
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((smem_u32(smem) & 1023) != 0) __trap();
   uint8_t* sKV = smem + 2 * kRegion;
@@ -1372,7 +1135,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const long long qpos = v.q_off + i;
       int jlo_row, jhi_row;
       row_bounds(s, v, qpos, jlo_row, jhi_row);
-      const float nslope2 = kAlibi ? -v.alibi[hq] * kLog2e : 0.f;
       uint8_t* sP = region((k + 1) & 1) + t * kTile;
       float m_ref = -INFINITY, l = 0.f;
       for (int j = R.lo; j < R.hi; ++j) {
@@ -1393,19 +1155,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool need_mask = !(j * BN >= R.jlo_last && (j + 1) * BN - 1 <= R.jhi_first);
         const int rel_lo = jlo_row - j * BN, rel_hi = jhi_row - j * BN;
         const float dq0 = (float)(qpos - v.kv_off - (long long)j * BN);
-        constexpr bool kAlibiLin = ATTN_ALIBI_LIN != 0 && kAlibi && !kSoftcap;
-        constexpr bool kCh = ATTN_CHUNK_MASK != 0;
-        float mt, e_off = 0.f;
-        if (kAlibiLin && ext_class(s, v, row0 + t * BM, j) != 0) {   // see score_tile_alibi_lin
-          const int cls = ext_class(s, v, row0 + t * BM, j);
-          e_off = (cls > 0 ? nslope2 : -nslope2) * dq0;
-          const float sslope = cls > 0 ? -nslope2 : nslope2;
-          mt = (need_mask ? score_tile_alibi_lin<true, kCh>(x, v, sslope, rel_lo, rel_hi)
-                          : score_tile_alibi_lin<false, kCh>(x, v, sslope, rel_lo, rel_hi)) + e_off;
-        } else {
-          mt = need_mask ? score_tile<kAlibi, kSoftcap, true, kCh>(x, v, nslope2, dq0, rel_lo, rel_hi)
-                         : score_tile<kAlibi, kSoftcap, false, kCh>(x, v, nslope2, dq0, rel_lo, rel_hi);
-        }
+        const float mt = need_mask ? score_tile<false, kSoftcap, true, true>(x, v, 0.f, dq0, rel_lo, rel_hi)
+                                   : score_tile<false, kSoftcap, false, true>(x, v, 0.f, dq0, rel_lo, rel_hi);
         const float m_run = fmaxf(m_ref, mt);
         bool move, need_o;
         if (m_ref == -INFINITY) {
@@ -1420,7 +1171,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (move) m_ref = m_run;
         l *= alpha;
         const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
-        const float e_add = e_off - m_use;   // (e_off: the ALiBi row constant of a uniform tile, else 0)
+        const float e_add = -m_use;
         if (n_pv > 0) {                 // PV_t of the previous step (maybe of the previous unit) is done
           mbar_wait(&o_done[t], (n_pv - 1) & 1);
           tc_fence_after();
@@ -1431,23 +1182,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint32_t pk[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
-            float a0, a1;
-            if constexpr (kF32x2) {
-              fma2_bc(a0, a1, x[c0 + 2 * e], x[c0 + 2 * e + 1], kPlain ? v.scale_log2 : 1.f, e_add);
-            } else if constexpr (kPlain) {
-              a0 = fmaf(x[c0 + 2 * e], v.scale_log2, e_add);
-              a1 = fmaf(x[c0 + 2 * e + 1], v.scale_log2, e_add);
-            } else {
-              a0 = x[c0 + 2 * e] + e_add;
-              a1 = x[c0 + 2 * e + 1] + e_add;
-            }
+            float a0, a1;   // exponent argument (log2 units), packed FFMA2
+            fma2_bc(a0, a1, x[c0 + 2 * e], x[c0 + 2 * e + 1], kPlain ? v.scale_log2 : 1.f, e_add);
             const float p0 = ex2_approx(a0), p1 = ex2_approx(a1);
-            if constexpr (kF32x2) {
-              add2_acc(sum0, sum1, p0, p1);
-            } else {
-              sum0 += p0;
-              sum1 += p1;
-            }
+            add2_acc(sum0, sum1, p0, p1);
             pk[e] = pack2<kF16>(p0, p1);
           }
           uint8_t* rowp = sP + (c0 >> 6) * (BM * 128) + r * 128;
@@ -1489,39 +1227,62 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&q_full[k & 1], (k >> 1) & 1);   // the Q tile we overwrite must have landed
         }
         const float inv_l = l > 0.f ? 1.f / l : 0.f;
+        if (s.o_part != nullptr) {   // fp32 normalised partial straight to global (no staging)
+          float* dst = s.o_part + (((size_t)un.zb * s.Hq + hq) * s.Sq + i) * D;
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t o[32];
-          if (n_it > 0) {
-            tmem_ld32(tO + c * 32, o);
-            tmem_ld_wait();
-          } else {
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t o[32];
+            if (n_it > 0) {
+              tmem_ld32(tO + c * 32, o);
+              tmem_ld_wait();
+            } else {
 #pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] = 0u;
+              for (int e = 0; e < 32; ++e) o[e] = 0u;
+            }
+            if (i < s.Sq) {
+#pragma unroll
+              for (int e = 0; e < 32; e += 4)
+                *reinterpret_cast<float4*>(dst + c * 32 + e) = make_float4(
+                    u2f(o[e]) * inv_l, u2f(o[e + 1]) * inv_l, u2f(o[e + 2]) * inv_l, u2f(o[e + 3]) * inv_l);
+            }
           }
-          uint32_t pk[16];
+          tc_fence_before();
+          if (tid_t == 0) mbar_arrive(&epi_done[k & 1]);
+        } else {
 #pragma unroll
-          for (int e = 0; e < 16; ++e) pk[e] = pack2<kF16>(u2f(o[2 * e]) * inv_l, u2f(o[2 * e + 1]) * inv_l);
-          uint8_t* rowp = sOut + (c >> 1) * (BM * 128) + r * 128;
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t o[32];
+            if (n_it > 0) {
+              tmem_ld32(tO + c * 32, o);
+              tmem_ld_wait();
+            } else {
 #pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            const int ch = (c & 1) * 4 + q4;
-            *reinterpret_cast<uint4*>(rowp + ((ch ^ (r & 7)) << 4)) =
-                make_uint4(pk[4 * q4], pk[4 * q4 + 1], pk[4 * q4 + 2], pk[4 * q4 + 3]);
+              for (int e = 0; e < 32; ++e) o[e] = 0u;
+            }
+            uint32_t pk[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) pk[e] = pack2<kF16>(u2f(o[2 * e]) * inv_l, u2f(o[2 * e + 1]) * inv_l);
+            uint8_t* rowp = sOut + (c >> 1) * (BM * 128) + r * 128;
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              const int ch = (c & 1) * 4 + q4;
+              *reinterpret_cast<uint4*>(rowp + ((ch ^ (r & 7)) << 4)) =
+                  make_uint4(pk[4 * q4], pk[4 * q4 + 1], pk[4 * q4 + 2], pk[4 * q4 + 3]);
+            }
           }
-        }
-        tc_fence_before();
-        fence_proxy_async_smem();
-        named_bar_sync(1 + t, kTileThreads);
-        if (tid_t == 0) {
-          for (int bx = 0; bx < 2; ++bx) tma_store_4d(&tm_o, sOut + bx * BM * 128, bx * 64, row0 + t * BM, hq, un.zb);
-          bulk_commit();
-          bulk_wait_read0();
-          mbar_arrive(&epi_done[k & 1]);
+          tc_fence_before();
+          fence_proxy_async_smem();
+          named_bar_sync(1 + t, kTileThreads);
+          if (tid_t == 0) {
+            for (int bx = 0; bx < 2; ++bx) tma_store_4d(&tm_o, sOut + bx * BM * 128, bx * 64, row0 + t * BM, hq, un.zb);
+            bulk_commit();
+            bulk_wait_read0();
+            mbar_arrive(&epi_done[k & 1]);
+          }
         }
         if (lse != nullptr && i < s.Sq)
           lse[((size_t)un.zb * s.Hq + hq) * s.Sq + i] = l > 0.f ? m_ref * kLn2 + logf(l) : -INFINITY;
-        named_bar_sync(1 + t, kTileThreads);   // the staging tile is free again (P of unit k+1 goes there)
+        if (s.o_part == nullptr) named_bar_sync(1 + t, kTileThreads);   // the staging tile is free again (P of unit k+1 goes there)
       } else if (tid_t == 0) {
         mbar_arrive(&epi_done[k & 1]);
       }
@@ -1545,28 +1306,28 @@ int sm_count_of_current_device() {
   return c;
 }
 
-template <bool kAlibi, bool kSoftcap, bool kF16>
+template <bool kSoftcap, bool kF16>
 cudaError_t launch_persist(const FwdTcArgs& a, cudaStream_t stream) {
   constexpr int kSmem = 4 * (2 * BM * 128 * 2) / 2 + 3 * (BN * 128 * 2) + 16 * 8 + 16;   // 2 regions + ring + bars
-  cudaError_t e = set_smem_once<fwd_tc_persist_kernel<kAlibi, kSoftcap, kF16>>(kSmem);
+  cudaError_t e = set_smem_once<fwd_tc_persist_kernel<kSoftcap, kF16>>(kSmem);
   if (e != cudaSuccess) return e;
   const long long nqb = (a.s.Sq + 2 * BM - 1) / (2 * BM);
   const long long units = nqb * a.s.Hq * a.s.B * (a.s.kv_splits > 1 ? a.s.kv_splits : 1);
   const int grid = (int)std::min<long long>(units, sm_count_of_current_device());
-  fwd_tc_persist_kernel<kAlibi, kSoftcap, kF16>
+  fwd_tc_persist_kernel<kSoftcap, kF16>
       <<<grid, kThreads, kSmem, stream>>>(a.tm_q, a.tm_k, a.tm_v, a.tm_o, a.s, a.v, a.lse);
   return cudaGetLastError();
 }
 
 template <int D, bool kAlibi, bool kSoftcap, bool kF16>
 cudaError_t launch_t(const FwdTcArgs& a, cudaStream_t stream) {
-  constexpr int NT = D == 128 ? ATTN_NT128 : ATTN_NT64;
+  constexpr int NT = nt_of<D>();
   using C = Cfg<D, alibi_mma<D, kAlibi && !kSoftcap>(), NT>;
   static_assert(C::kSmemBytes <= 232448, "shared memory");
-  if constexpr (D == 128 && NT == 2 && C::kPS && kHalves == 1 && !kTraceBuild) {
-    const bool pure_causal = a.v.causal && a.v.window_left < 0 && a.v.window_right < 0;
-    // (ALiBi stays on the grid kernel: it walks the KV tiles diagonal-first, see J in fwd_tc_kernel)
-    if (ATTN_PERSIST == 2 || (ATTN_PERSIST == 1 && pure_causal && !kAlibi)) return launch_persist<kAlibi, kSoftcap, kF16>(a, stream);
+  if constexpr (D == 128 && !kAlibi && !kTraceBuild) {
+    // pure causal -> the persistent kernel (ALiBi stays on the grid kernel: it walks the KV
+    // tiles diagonal-first, see J in fwd_tc_kernel)
+    if (a.v.causal && a.v.window_left < 0 && a.v.window_right < 0) return launch_persist<kSoftcap, kF16>(a, stream);
   }
   auto kern = fwd_tc_kernel<D, kAlibi, kSoftcap, kF16, NT>;
   cudaError_t e = set_smem_once<fwd_tc_kernel<D, kAlibi, kSoftcap, kF16, NT>>(C::kSmemBytes);

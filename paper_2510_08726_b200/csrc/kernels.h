@@ -44,6 +44,10 @@ struct Shape {
   // owning KV tiles [s*kv_split_tiles, (s+1)*kv_split_tiles); outputs go to batch index
   // s*B + b of a partial [kv_splits*B] output.  kv_splits <= 1: off.
   int kv_splits = 1, kv_split_tiles = 0;
+  // fp32 output of normalised partials (KV split, context-parallel prefill): when set the
+  // prefill kernels write O / l as fp32 [kv_splits*B][Hq][Sq][D] (dense) here instead of
+  // storing the 16-bit output through tm_o.
+  float* o_part = nullptr;
 };
 
 // ------------------------------------------------------------ tcgen05 prefill

@@ -81,9 +81,10 @@ def decode_kv_sharded(q: torch.Tensor, k_shard: torch.Tensor, v_shard: torch.Ten
 
 # ----------------------------------------------------------------------------- context-parallel prefill (NEXT-3)
 def _prefill_local(q, k_shard, v_shard, *, kv_pos_offset, seqlen_kv_total, variant):
-    from . import fused_fwd
-    return fused_fwd(q, k_shard, v_shard, kv_pos_offset=kv_pos_offset, seqlen_kv_total=seqlen_kv_total,
-                     return_lse=True, **variant)
+    from . import fused_fwd_partial
+    # fp32 normalised partial: the gathered (O_r, lse_r) carry no 16-bit rounding into Eq. 8
+    return fused_fwd_partial(q, k_shard, v_shard, kv_pos_offset=kv_pos_offset, seqlen_kv_total=seqlen_kv_total,
+                             **variant)
 
 
 def prefill_kv_sharded(q: torch.Tensor, k_shard: torch.Tensor, v_shard: torch.Tensor, *, kv_pos_offset: int,
@@ -179,12 +180,17 @@ class NcclComm:
                         window=variant.get("window", (-1, -1)), alibi_slopes=variant.get("alibi_slopes"),
                         softcap=variant.get("softcap", 0.0), q_pos_offset=variant.get("q_pos_offset"),
                         kv_pos_offset=kv_pos_offset, seqlen_kv_total=seqlen_kv_total)
+        from . import _check_io, _torch_stream
         need = lib.attn_decode_kv_sharded_workspace_bytes(ctypes.byref(prob), self.world)
-        if workspace is None or workspace.numel() * workspace.element_size() < need:
-            workspace = torch.empty(need, dtype=torch.uint8, device=q.device)
+        if workspace is None:
+            with torch.cuda.stream(_torch_stream(q.device, stream)):
+                workspace = torch.empty(need, dtype=torch.uint8, device=q.device)
+        elif workspace.numel() * workspace.element_size() < need or workspace.device != q.device:
+            raise ValueError(f"workspace must be >= {need} bytes on q's device")
         if out is None:
             out = torch.empty_like(q, memory_format=torch.contiguous_format)
         lse = torch.empty(q.shape[:2], device=q.device, dtype=torch.float32) if return_lse else None
+        _check_io(q, k_shard, v_shard, out, lse, q.shape[:2])
         check(lib.attn_decode_kv_sharded(self._h, ctypes.byref(prob), _as_tensor(q), _as_tensor(k_shard),
                                          _as_tensor(v_shard), workspace.data_ptr(),
                                          workspace.numel() * workspace.element_size(), _as_tensor(out),

@@ -100,22 +100,31 @@ def variant_no_slopes(v):
 
 
 # --------------------------------------------------------------------------- context-parallel prefill (NEXT-3)
-@pytest.mark.parametrize("W,variant", [(2, dict(causal=True)), (3, dict(causal=True, window_left=300)),
-                                       (4, dict())])
-def test_kv_sharded_prefill_loopback(W, variant):
-    B, Hq, Hkv, S, D = 1, 4, 2, 700, 128
+@pytest.mark.parametrize("W,variant,D", [(2, dict(causal=True), 128), (3, dict(causal=True, window_left=300), 128),
+                                         (4, dict(), 128), (3, dict(causal=True), 64)])
+def test_kv_sharded_prefill_loopback(W, variant, D):
+    """Context-parallel prefill: every shard's fp32 normalised partial (attn_fused_fwd_partial)
+    equals the oracle restricted to the shard's keys (absolute positions), and Eq. 8 over
+    the shards equals the oracle over all keys."""
+    B, Hq, Hkv, S = 1, 4, 2, 700
     kw = dict(variant)
     p = problem(B, Hq, Hkv, S, S, D, **kw)
     raw, f64 = gen_qkv(1200 + W, B, Hq, Hkv, S, S, D)
     ref_o, ref_l = oracle.attention(p, *f64)
     q, k, v = (dgd.to_device(x) for x in raw)
     win = (kw.pop("window_left", -1), -1)
-    o_all = torch.empty(W, B, Hq, S, D, dtype=torch.bfloat16, device="cuda")
+    o_all = torch.empty(W, B, Hq, S, D, dtype=torch.float32, device="cuda")
     lse_all = torch.empty(W, B, Hq, S, device="cuda")
     for r in range(W):
         lo, hi = pdist.shard_range(S, r, W)
         o_r, l_r = pdist._prefill_local(q, k[:, :, lo:hi].contiguous(), v[:, :, lo:hi].contiguous(),
                                         kv_pos_offset=lo, seqlen_kv_total=S, variant=dict(window=win, **kw))
+        assert o_r.dtype == torch.float32
+        pr = problem(B, Hq, Hkv, S, hi - lo, D, kv_pos_offset=lo, seqlen_kv_total=S, q_pos_offset=0,
+                     window_left=win[0], **kw)
+        ro, rl = oracle.attention(pr, f64[0], f64[1][:, :, lo:hi], f64[2][:, :, lo:hi])
+        assert_bf16_close(o_r.cpu().numpy().astype(np.float64), ro, f"CP partial W={W} r={r}")
+        assert_lse_close(l_r.cpu().numpy(), rl, LSE_TOL_BF16, f"CP partial lse W={W} r={r}")
         o_all[r].copy_(o_r)
         lse_all[r].copy_(l_r)
     out, lse = pdist.merge_prefill_parts(o_all, lse_all, torch.bfloat16)

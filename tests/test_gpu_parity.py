@@ -326,9 +326,11 @@ def test_decode_parts_and_output(case):
             assert metrics(go[:, b, hq], po[:, 0])[1] < 5e-3
 
 
-@pytest.mark.parametrize("B", [1, 4])
+@pytest.mark.parametrize("B", [1, 4, 8, 16])
 def test_decode_full_config_sampled(B):
-    """Config 5: Hq=32, Hkv=8, KV 128K, D=128, causal (all keys), auto splits."""
+    """Config 5: Hq=32, Hkv=8, KV 128K, D=128, causal (all keys), auto splits -- the split
+    count bench.py times (B >= 8: >= 64 (b, hkv) groups, so the count rounds up to <= 2
+    CTAs per SM, csrc/api.cu attn_splitkv_default_splits)."""
     Hq, Hkv, L, D = 32, 8, 131072, 128
     p = problem(B, Hq, Hkv, 1, L, D, causal=True)
     seed = datagen.config_seed(5)
