@@ -223,6 +223,20 @@ ATTN_API attn_status attn_splitkv_decode(const attn_problem* prob, attn_tensor q
                                 const attn_parts* parts_out, attn_tensor o, float* lse,
                                 attn_stream_t stream);
 
+/* attn_splitkv_decode_packed: the same local section with the fused global
+ * section (Eq. 8 over the splits, last CTA per (b, hkv)) writing the UN-normalised
+ * merged triple of every (b, hq) instead of O / lse:
+ *   packed[(b*Hq + hq)*(D+2) + d] = sum_s w_s O_s[d]   (d < D),
+ *   packed[... + D] = M (natural log; -inf if no key),  packed[... + D + 1] = L,
+ * with M = max_s m_s, w_s = exp(m_s - M), L = sum_s w_s l_s -- the send buffer of
+ * a KV-sharded decode (one launch).  seqlen_q must be 1; workspace as for
+ * attn_splitkv_decode (ticket block zero); num_splits must not exceed the
+ * kernel's staging limit (UNSUPPORTED otherwise; 0 = default, always within).
+ * packed: DEVICE fp32 [B][Hq][D+2] contiguous. */
+ATTN_API attn_status attn_splitkv_decode_packed(const attn_problem* prob, attn_tensor q, attn_tensor k,
+                                                attn_tensor v, int32_t num_splits, void* workspace,
+                                                size_t workspace_bytes, float* packed, attn_stream_t stream);
+
 /* ---------------------------------------------------------------------
  * attn_combine -- the Split-K global section (Fig. 5 s_max_global /
  * s_sum_global, Eq. 8) over in->num_parts partial triples per
@@ -290,19 +304,24 @@ ATTN_API attn_status attn_softmax_rows(int64_t rows, int32_t cols, attn_dtype dt
  *   nranks processes; this process is `rank`; the CURRENT CUDA device is
  *   used.  Blocks until all ranks joined (ncclCommInitRank).
  * attn_nccl_comm_destroy: frees the handle (NULL is a no-op).
- * attn_decode_kv_sharded_workspace_bytes: DEVICE workspace for the call below.
+ * attn_decode_kv_sharded_workspace_bytes: DEVICE workspace for the call below
+ *   (256-byte aligned).  Its first 256-byte-rounded [B][Hkv] uint32 block holds
+ *   the decode kernel's arrival tickets and MUST be zero before the first call
+ *   (every call leaves it zero, as for attn_splitkv_decode).
  * attn_decode_kv_sharded: `local` describes THIS rank's shard: seqlen_kv =
  *   shard length, kv_pos_offset = absolute position of the shard's first key,
  *   seqlen_kv_total = global KV length; q is replicated on every rank.  Steps,
- *   all enqueued on `stream`:
- *     1. attn_splitkv_decode over the shard -> split triples (workspace);
- *     2. attn_combine -> one UN-normalised triple per (b, hq), packed as
- *        [B][Hq][D+2] fp32 (O at 0..D-1, m at D, l at D+1);
- *     3. ncclAllGather -> [nranks][B][Hq][D+2];
- *     4. attn_combine over the nranks parts -> o (q's dtype), lse (nullable,
+ *   all enqueued on `stream` (CUDA-graph capturable):
+ *     1. attn_splitkv_decode_packed over the shard: the split kernel's fused
+ *        global section merges this rank's splits into one UN-normalised
+ *        triple per (b, hq), packed as [B][Hq][D+2] fp32 (O at 0..D-1, m at D,
+ *        l at D+1) -- one launch (a separate merge launch only when the split
+ *        count exceeds what the kernel can stage);
+ *     2. ncclAllGather -> [nranks][B][Hq][D+2];
+ *     3. attn_combine over the nranks parts -> o (q's dtype), lse (nullable,
  *        fp32 [B][Hq]) -- identical on every rank.
  *   Errors: those of attn_splitkv_decode / attn_combine, WORKSPACE_TOO_SMALL,
- *   NCCL.
+ *   ALIGNMENT, NCCL.
  * ------------------------------------------------------------------- */
 ATTN_API attn_status attn_nccl_get_unique_id(void* id_out);
 ATTN_API attn_status attn_nccl_comm_init(void** comm, int32_t nranks, int32_t rank, const void* nccl_unique_id);

@@ -308,14 +308,18 @@ def splitkv_decode(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, num_spl
                    q_pos_offset: Optional[int] = None, kv_pos_offset: int = 0,
                    seqlen_kv_total: Optional[int] = None, out: Optional[torch.Tensor] = None,
                    lse: Optional[torch.Tensor] = None, return_lse: bool = False, parts: Optional[Parts] = None,
-                   workspace: Optional[torch.Tensor] = None, want_out: bool = True, stream=None):
+                   workspace: Optional[torch.Tensor] = None, want_out: bool = True,
+                   packed: Optional[torch.Tensor] = None, stream=None):
     """Split-K Update decode (``attn_splitkv_decode``): q [B, Hq, Sq, D] bf16/fp16 with
     Sq = 1, or a few query tokens (multi-token decode) with G * Sq <= 16 packed rows.
 
     ``parts`` receives the raw local-section triples; with ``want_out`` the
     Eq. 8 combine also produces O (and lse) -- fused into the split kernel
-    when ``parts`` is None.  A caller-supplied ``workspace`` must be zeroed
-    before its first use (its ticket block; include/attn.h)."""
+    when ``parts`` is None.  ``packed`` (fp32 [B, Hq, D + 2], Sq = 1): the fused
+    combine writes the UN-normalised merged triple there instead
+    (``attn_splitkv_decode_packed``; returns ``packed``).  A caller-supplied
+    ``workspace`` must be zeroed before its first use (its ticket block;
+    include/attn.h)."""
     lib = load()
     if q.device.type == "cpu":
         dev = torch.device("cuda", torch.cuda.current_device())
@@ -332,6 +336,22 @@ def splitkv_decode(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, num_spl
                     q_pos_offset=q_pos_offset, kv_pos_offset=kv_pos_offset, seqlen_kv_total=seqlen_kv_total)
     if num_splits == 0:
         num_splits = lib.attn_splitkv_default_splits(ctypes.byref(prob), 0)
+    if packed is not None:
+        B, Hq, Sq, D = q.shape
+        _check_io(q, k, v)
+        if Sq != 1 or packed.dtype != torch.float32 or tuple(packed.shape) != (B, Hq, D + 2) \
+                or not packed.is_contiguous() or packed.device != q.device:
+            raise ValueError(f"packed must be a contiguous float32 [{B}, {Hq}, {D + 2}] tensor (Sq = 1)")
+        need = lib.attn_splitkv_workspace_bytes(ctypes.byref(prob), num_splits)
+        if workspace is None:
+            workspace = _decode_workspace(q.device, need, (B * k.shape[1] * 4 + 255) // 256 * 256, stream)
+        elif workspace.numel() * workspace.element_size() < need or workspace.device != q.device:
+            raise ValueError(f"workspace must be >= {need} bytes on q's device")
+        check(lib.attn_splitkv_decode_packed(ctypes.byref(prob), _as_tensor(q), _as_tensor(k), _as_tensor(v),
+                                             num_splits, workspace.data_ptr(),
+                                             workspace.numel() * workspace.element_size(), packed.data_ptr(),
+                                             _stream(stream)), "attn_splitkv_decode_packed")
+        return packed
     if want_out and out is None:
         out = torch.empty_like(q, memory_format=torch.contiguous_format)
     if not want_out:

@@ -27,7 +27,7 @@ EXPORTED = ("attn_fused_fwd", "attn_splitkv_default_splits", "attn_splitkv_works
             "attn_nccl_get_unique_id", "attn_nccl_comm_init", "attn_nccl_comm_destroy",
             "attn_decode_kv_sharded_workspace_bytes", "attn_decode_kv_sharded",
             "attn_fused_fwd_default_splits", "attn_fused_fwd_workspace_bytes", "attn_fused_fwd_splitkv",
-            "attn_debug_repair_counters", "attn_fused_fwd_partial")
+            "attn_debug_repair_counters", "attn_fused_fwd_partial", "attn_splitkv_decode_packed")
 # repair-event counter slots (include/attn.h ATTN_REPAIR_*)
 ATTN_REPAIR_FWD128, ATTN_REPAIR_FWD64, ATTN_REPAIR_PERSIST, ATTN_REPAIR_DECODE = 0, 1, 2, 3
 ATTN_REPAIR_SLOTS = 4
@@ -101,6 +101,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.attn_splitkv_workspace_bytes.restype = ctypes.c_size_t
     lib.attn_splitkv_decode.argtypes = [P, T, T, T, i32, vp, ctypes.c_size_t, Pa, T, f32p, vp]
     lib.attn_splitkv_decode.restype = ctypes.c_int
+    lib.attn_splitkv_decode_packed.argtypes = [P, T, T, T, i32, vp, ctypes.c_size_t, vp, vp]
+    lib.attn_splitkv_decode_packed.restype = ctypes.c_int
     lib.attn_combine.argtypes = [i32, i32, i32, Pa, ctypes.c_int, T, f32p, Pa, vp]
     lib.attn_combine.restype = ctypes.c_int
     i64 = ctypes.c_int64

@@ -343,9 +343,14 @@ size_t attn_splitkv_workspace_bytes(const attn_problem* p, int32_t num_splits) {
   return up((size_t)p->batch * p->heads_kv * 4) + up(rows * 4) * 2 + up(rows * p->head_dim * 4);
 }
 
-attn_status attn_splitkv_decode(const attn_problem* prob, attn_tensor q, attn_tensor k, attn_tensor v,
-                                int32_t num_splits, void* workspace, size_t workspace_bytes,
-                                const attn_parts* parts_out, attn_tensor o, float* lse, attn_stream_t stream) {
+}  // extern "C"
+
+namespace {
+// attn_splitkv_decode, and (packed != NULL) its fused form that ends in the un-normalised
+// packed triple of attn_splitkv_decode_packed.
+attn_status decode_impl(const attn_problem* prob, attn_tensor q, attn_tensor k, attn_tensor v, int32_t num_splits,
+                        void* workspace, size_t workspace_bytes, const attn_parts* parts_out, attn_tensor o,
+                        float* lse, float* packed, attn_stream_t stream) {
   g_err[0] = 0;
   attn::VariantParams vp;
   attn_status st = check_problem(prob, &vp);
@@ -360,7 +365,9 @@ attn_status attn_splitkv_decode(const attn_problem* prob, attn_tensor q, attn_te
   if ((int64_t)G * Sq > 16)
     return fail(ATTN_ERR_UNSUPPORTED, "decode packs G * seqlen_q <= 16 rows (got %d x %d); use attn_fused_fwd",
                 G, Sq);
-  CHECK_ARG(parts_out != nullptr || o.ptr != nullptr, "decode needs parts_out or o");
+  CHECK_ARG(parts_out != nullptr || o.ptr != nullptr || packed != nullptr, "decode needs parts_out or o");
+  if (packed != nullptr && (Sq != 1 || parts_out != nullptr || o.ptr != nullptr))
+    return fail(ATTN_ERR_UNSUPPORTED, "the packed triple output needs seqlen_q == 1 and no other output");
   if (Sq > 1 && parts_out != nullptr)
     return fail(ATTN_ERR_UNSUPPORTED, "parts_out (a per-(b, h) triple) needs seqlen_q == 1");
   if (num_splits < 0) return fail(ATTN_ERR_INVALID_ARGUMENT, "num_splits must be >= 0");
@@ -409,7 +416,7 @@ attn_status attn_splitkv_decode(const attn_problem* prob, attn_tensor q, attn_te
                               (long long)p.heads_q * Sq * p.head_dim, (long long)Sq * p.head_dim};
     // Fused Eq. 8 combine (last CTA per (b, hkv)) when the output is wanted and the
     // split weights fit the kernel's staging area; else the separate combine kernel.
-    if (o.ptr != nullptr && num_splits <= attn::decode_fused_max_splits(G * Sq, p.head_dim)) {
+    if ((o.ptr != nullptr || packed != nullptr) && num_splits <= attn::decode_fused_max_splits(G * Sq, p.head_dim)) {
       a.tickets = reinterpret_cast<unsigned*>(w0);
       a.out_f16 = p.dtype == ATTN_FP16 ? 1 : 0;
       a.o = o.ptr;
@@ -417,6 +424,10 @@ attn_status attn_splitkv_decode(const attn_problem* prob, attn_tensor q, attn_te
       a.o_sh = o.stride_h;
       a.o_ss = o.stride_s;
       a.lse = lse;
+      a.packed = packed;
+    } else if (packed != nullptr) {
+      return fail(ATTN_ERR_UNSUPPORTED, "packed output needs num_splits <= %d",
+                  attn::decode_fused_max_splits(G * Sq, p.head_dim));
     }
   }
   if ((st = make_map(&a.tm_k, k, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, nk, true, a.f16)) != ATTN_OK) return st;
@@ -441,6 +452,26 @@ attn_status attn_splitkv_decode(const attn_problem* prob, attn_tensor q, attn_te
   }
   if (st == ATTN_OK) g_launches = launches;
   return st;
+}
+}  // namespace
+
+extern "C" {
+
+attn_status attn_splitkv_decode(const attn_problem* prob, attn_tensor q, attn_tensor k, attn_tensor v,
+                                int32_t num_splits, void* workspace, size_t workspace_bytes,
+                                const attn_parts* parts_out, attn_tensor o, float* lse, attn_stream_t stream) {
+  return decode_impl(prob, q, k, v, num_splits, workspace, workspace_bytes, parts_out, o, lse, nullptr, stream);
+}
+
+attn_status attn_splitkv_decode_packed(const attn_problem* prob, attn_tensor q, attn_tensor k, attn_tensor v,
+                                       int32_t num_splits, void* workspace, size_t workspace_bytes, float* packed,
+                                       attn_stream_t stream) {
+  if (packed == nullptr) {
+    g_err[0] = 0;
+    return fail(ATTN_ERR_INVALID_ARGUMENT, "packed is NULL");
+  }
+  const attn_tensor none{nullptr, 0, 0, 0};
+  return decode_impl(prob, q, k, v, num_splits, workspace, workspace_bytes, nullptr, none, nullptr, packed, stream);
 }
 
 attn_status attn_combine(int32_t batch, int32_t heads, int32_t head_dim, const attn_parts* in,
@@ -603,9 +634,9 @@ attn_status attn_nccl_comm_destroy(void* comm) {
 size_t attn_decode_kv_sharded_workspace_bytes(const attn_problem* p, int32_t nranks) {
   if (p == nullptr || nranks < 1) return 0;
   const int32_t splits = attn_splitkv_default_splits(p, 0);
-  const size_t rows = (size_t)splits * p->batch * p->heads_q;
   const size_t packed = (size_t)p->batch * p->heads_q * (p->head_dim + 2);
-  return up256(rows * 4) * 2 + up256(rows * p->head_dim * 4) + up256(packed * 4) * (1 + (size_t)nranks);
+  // [split-decode workspace: tickets | m | l | O] [send: packed triples] [recv: nranks x packed]
+  return attn_splitkv_workspace_bytes(p, splits) + up256(packed * 4) * (1 + (size_t)nranks);
 }
 
 attn_status attn_decode_kv_sharded(void* comm, const attn_problem* local, attn_tensor q, attn_tensor k_shard,
@@ -618,32 +649,44 @@ attn_status attn_decode_kv_sharded(void* comm, const attn_problem* local, attn_t
   const size_t need = attn_decode_kv_sharded_workspace_bytes(local, c->nranks);
   if (workspace == nullptr || workspace_bytes < need)
     return fail(ATTN_ERR_WORKSPACE_TOO_SMALL, "workspace needs %zu bytes", need);
+  if ((reinterpret_cast<uintptr_t>(workspace) & 255) != 0)
+    return fail(ATTN_ERR_ALIGNMENT, "workspace must be 256-byte aligned");
   const attn_problem& p = *local;
   const int32_t splits = attn_splitkv_default_splits(local, 0);
-  const size_t rows = (size_t)splits * p.batch * p.heads_q;
+  const size_t dec_ws = attn_splitkv_workspace_bytes(local, splits);
   const long long bh = (long long)p.batch * p.heads_q, D = p.head_dim, W = D + 2;
   char* w = static_cast<char*>(workspace);
-  float* pm = reinterpret_cast<float*>(w);
-  float* pl = reinterpret_cast<float*>(w + up256(rows * 4));
-  float* po = reinterpret_cast<float*>(w + 2 * up256(rows * 4));
-  float* send = reinterpret_cast<float*>(w + 2 * up256(rows * 4) + up256(rows * D * 4));
+  float* send = reinterpret_cast<float*>(w + dec_ws);
   float* recv = reinterpret_cast<float*>(reinterpret_cast<char*>(send) + up256(bh * W * 4));
-  // 1. local section over this rank's keys
-  const attn_parts parts{pm, pl, po, splits, bh, p.heads_q, 1, bh * D, (int64_t)p.heads_q * D, D};
   const attn_tensor none{nullptr, 0, 0, 0};
-  attn_status st = attn_splitkv_decode(local, q, k_shard, v_shard, splits, nullptr, 0, &parts, none, nullptr, stream);
-  if (st != ATTN_OK) return st;
-  int launches = g_launches;
-  // 2. this rank's splits -> one un-normalised triple per (b, hq), packed [B][Hq][D+2]
-  const attn_parts packed{send + D, send + D + 1, send, 1, 0, p.heads_q * W, W, 0, p.heads_q * W, W};
-  st = attn_combine(p.batch, p.heads_q, p.head_dim, &parts, p.dtype, none, nullptr, &packed, stream);
-  if (st != ATTN_OK) return st;
-  launches += g_launches;
-  // 3. all-gather the packed triples
+  int launches = 0;
+  attn_status st;
+  // 1. local section over this rank's keys, its splits merged by the fused global section of the
+  //    same launch into one UN-normalised triple per (b, hq), packed [B][Hq][D+2] (send buffer)
+  if (splits <= attn::decode_fused_max_splits(p.heads_q / p.heads_kv, p.head_dim)) {
+    st = decode_impl(local, q, k_shard, v_shard, splits, w, dec_ws, nullptr, none, nullptr, send, stream);
+    if (st != ATTN_OK) return st;
+    launches = g_launches;
+  } else {   // too many splits to stage in the kernel: raw triples, then a separate merge
+    const size_t rows = (size_t)splits * p.batch * p.heads_q;
+    char* w1 = w + up256((size_t)p.batch * p.heads_kv * 4);
+    float* pm = reinterpret_cast<float*>(w1);
+    float* pl = reinterpret_cast<float*>(w1 + up256(rows * 4));
+    float* po = reinterpret_cast<float*>(w1 + 2 * up256(rows * 4));
+    const attn_parts parts{pm, pl, po, splits, bh, p.heads_q, 1, bh * D, (int64_t)p.heads_q * D, D};
+    st = decode_impl(local, q, k_shard, v_shard, splits, nullptr, 0, &parts, none, nullptr, nullptr, stream);
+    if (st != ATTN_OK) return st;
+    launches = g_launches;
+    const attn_parts packed{send + D, send + D + 1, send, 1, 0, p.heads_q * W, W, 0, p.heads_q * W, W};
+    st = attn_combine(p.batch, p.heads_q, p.head_dim, &parts, p.dtype, none, nullptr, &packed, stream);
+    if (st != ATTN_OK) return st;
+    launches += g_launches;
+  }
+  // 2. all-gather the packed triples
   st = nccl_status(nccl().all_gather(send, recv, (size_t)bh * W, kNcclFloat32, c->nc,
                                      reinterpret_cast<cudaStream_t>(stream)), "ncclAllGather");
   if (st != ATTN_OK) return st;
-  // 4. Eq. 8 over the ranks' triples
+  // 3. Eq. 8 over the ranks' triples
   const attn_parts gathered{recv + D, recv + D + 1, recv, c->nranks, bh * W, p.heads_q * W, W,
                             bh * W, p.heads_q * W, W};
   st = attn_combine(p.batch, p.heads_q, p.head_dim, &gathered, p.dtype, o, lse, nullptr, stream);

@@ -409,6 +409,18 @@ __global__ void __launch_bounds__(kThreads) decode_split_kernel(const __grid_con
         }
       }
     }
+    if (a.packed != nullptr) {   // un-normalised triple for a further Eq. 8 merge (KV-sharded decode)
+      float* row = a.packed + ((long long)b * a.s.Hq + hh) * (D + 2);
+      row[d] = acc.x;
+      row[d + 1] = acc.y;
+      row[d + 2] = acc.z;
+      row[d + 3] = acc.w;
+      if (d == 0) {
+        row[D] = L > 0.f ? stat[rho * 2] : -INFINITY;
+        row[D + 1] = L;
+      }
+      continue;
+    }
     const float inv = L > 0.f ? 1.f / L : 0.f;
     const float out[4] = {acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv};
     const long long oi = (long long)b * a.o_sb + (long long)hh * a.o_sh + (long long)qi * a.o_ss + d;

@@ -91,6 +91,10 @@ struct DecodeArgs {
   int out_f16;                  // output dtype: 1 fp16, 0 bf16
   void* o; long long o_sb, o_sh, o_ss;
   float* lse;                   // nullable [B][Hq][Sq]
+  // packed != nullptr (Sq == 1): the fused global section writes the UN-normalised merged
+  // triple of each (b, hq) -- O_acc at [0, D), m (natural log) at D, l at D + 1 of row
+  // (b * Hq + hq) * (D + 2) -- instead of O / lse (the send buffer of the KV-sharded decode).
+  float* packed;
 };
 cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t stream, int* launches);
 int decode_stage_keys(int G, int D);

@@ -65,15 +65,21 @@ def decode_kv_sharded(q: torch.Tensor, k_shard: torch.Tensor, v_shard: torch.Ten
     k_shard/v_shard [B, Hkv, L_r, D] hold keys [kv_pos_offset, kv_pos_offset + L_r)
     of a sequence of seqlen_kv_total keys.  Returns O [B, Hq, 1, D] (and lse)
     on every rank."""
-    local = local or _local_kernels
-    merge = merge or _merge_kernels
     final = final or _final_kernels
     world = dist.get_world_size(group)
     B, Hq, _, D = q.shape
-    parts = local(q, k_shard, v_shard, kv_pos_offset=kv_pos_offset, seqlen_kv_total=seqlen_kv_total,
-                  num_splits=num_splits, variant=variant)
     send = torch.empty(1, B, Hq, D + 2, dtype=torch.float32, device=q.device)
-    merge(parts, Parts.packed(send))
+    if local is None and merge is None:
+        # one launch: the split kernel's fused Eq. 8 section writes this rank's merged,
+        # un-normalised triples straight into the send buffer
+        splitkv_decode(q, k_shard, v_shard, num_splits=num_splits, packed=send[0], kv_pos_offset=kv_pos_offset,
+                       seqlen_kv_total=seqlen_kv_total, **variant)
+    else:
+        local = local or _local_kernels
+        merge = merge or _merge_kernels
+        parts = local(q, k_shard, v_shard, kv_pos_offset=kv_pos_offset, seqlen_kv_total=seqlen_kv_total,
+                      num_splits=num_splits, variant=variant)
+        merge(parts, Parts.packed(send))
     recv = torch.empty(world, B, Hq, D + 2, dtype=torch.float32, device=q.device)
     dist.all_gather_into_tensor(recv, send, group=group)
     return final(Parts.packed(recv), q.dtype, return_lse)
@@ -171,7 +177,8 @@ class NcclComm:
                           return_lse: bool = False, workspace: Optional[torch.Tensor] = None, stream=None,
                           **variant):
         """``attn_decode_kv_sharded`` on this communicator (same contract as
-        :func:`decode_kv_sharded`; identical O, lse on every rank)."""
+        :func:`decode_kv_sharded`; identical O, lse on every rank).  A caller-supplied
+        ``workspace`` must be zeroed before its first use (include/attn.h)."""
         import ctypes
         from . import _as_tensor, _problem, _stream
         from ._ffi import check, load
@@ -182,11 +189,14 @@ class NcclComm:
                         kv_pos_offset=kv_pos_offset, seqlen_kv_total=seqlen_kv_total)
         from . import _check_io, _torch_stream
         need = lib.attn_decode_kv_sharded_workspace_bytes(ctypes.byref(prob), self.world)
-        if workspace is None:
-            with torch.cuda.stream(_torch_stream(q.device, stream)):
-                workspace = torch.empty(need, dtype=torch.uint8, device=q.device)
+        if workspace is None:   # cached per communicator; zeroed once (its ticket block), left zero by every call
+            ws = getattr(self, "_ws", None)
+            if ws is None or ws.numel() < need or ws.device != q.device:
+                with torch.cuda.stream(_torch_stream(q.device, stream)):
+                    self._ws = torch.zeros(need, dtype=torch.uint8, device=q.device)
+            workspace = self._ws
         elif workspace.numel() * workspace.element_size() < need or workspace.device != q.device:
-            raise ValueError(f"workspace must be >= {need} bytes on q's device")
+            raise ValueError(f"workspace must be >= {need} bytes on q's device (zeroed before first use)")
         if out is None:
             out = torch.empty_like(q, memory_format=torch.contiguous_format)
         lse = torch.empty(q.shape[:2], device=q.device, dtype=torch.float32) if return_lse else None

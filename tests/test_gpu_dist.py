@@ -24,8 +24,13 @@ if torch.cuda.is_available():
     from paper_2510_08726_b200 import dist as pdist
 
 
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("W", [2, 3, 8])
-def test_kv_sharded_decode_loopback(W):
+def test_kv_sharded_decode_loopback(W, fused):
+    """fused: each shard's split kernel writes its merged un-normalised triple straight into
+    the packed send slot (attn_splitkv_decode_packed, one launch); else raw split triples +
+    a separate attn_combine(acc_out).  Each shard's packed (m, l) must give the oracle's lse
+    over the shard's keys; Eq. 8 over the W slots must give the unsharded oracle."""
     B, Hq, Hkv, L, D = 2, 8, 2, 3001, 128
     p = problem(B, Hq, Hkv, 1, L, D, causal=True)
     raw, f64 = gen_qkv(900 + W, B, Hq, Hkv, 1, L, D)
@@ -34,9 +39,19 @@ def test_kv_sharded_decode_loopback(W):
     packed = torch.empty(W, B, Hq, D + 2, device="cuda")
     for r in range(W):
         lo, hi = pdist.shard_range(L, r, W)
-        parts = pdist._local_kernels(q, k[:, :, lo:hi].contiguous(), v[:, :, lo:hi].contiguous(), kv_pos_offset=lo,
-                                     seqlen_kv_total=L, num_splits=0, variant=dict(causal=True))
-        pdist._merge_kernels(parts, pb.Parts.packed(packed[r:r + 1]))
+        ks, vs = k[:, :, lo:hi].contiguous(), v[:, :, lo:hi].contiguous()
+        if fused:
+            pb.splitkv_decode(q, ks, vs, packed=packed[r], kv_pos_offset=lo, seqlen_kv_total=L, causal=True)
+            torch.cuda.synchronize()
+            assert pb.last_launch_count() == 1
+        else:
+            parts = pdist._local_kernels(q, ks, vs, kv_pos_offset=lo, seqlen_kv_total=L, num_splits=0,
+                                         variant=dict(causal=True))
+            pdist._merge_kernels(parts, pb.Parts.packed(packed[r:r + 1]))
+        ps = problem(B, Hq, Hkv, 1, hi - lo, D, causal=True, seqlen_kv_total=L, q_pos_offset=L - 1, kv_pos_offset=lo)
+        _, rl = oracle.attention(ps, f64[0], f64[1][:, :, lo:hi], f64[2][:, :, lo:hi])
+        pk = packed[r].cpu().numpy().astype(np.float64)
+        assert_lse_close(pk[..., D] + np.log(pk[..., D + 1]), rl[:, :, 0], LSE_TOL_BF16, f"shard {r} (m, l)")
     out, lse = pdist._final_kernels(pb.Parts.packed(packed), torch.bfloat16, True)
     assert_bf16_close(out.float().cpu().numpy().astype(np.float64), ref_o, f"W={W}")
     assert_lse_close(lse.cpu().numpy(), ref_l[:, :, 0], LSE_TOL_BF16, "lse")
@@ -80,7 +95,7 @@ def test_kv_sharded_decode_c_abi_one_rank(variant):
     try:
         out, lse = comm.decode_kv_sharded(q, k, v, kv_pos_offset=0, seqlen_kv_total=L, return_lse=True, **variant)
         torch.cuda.synchronize()
-        assert pb.last_launch_count() == 3            # decode + local merge + final combine (+ NCCL)
+        assert pb.last_launch_count() == 2            # decode with fused local merge + final combine (+ NCCL)
         assert_bf16_close(out.float().cpu().numpy().astype(np.float64), ref_o, f"C-ABI kv-sharded {variant}")
         assert_lse_close(lse.cpu().numpy(), ref_l[:, :, 0], LSE_TOL_BF16, "C-ABI kv-sharded lse")
         # a shard holding keys [lo, L) of the sequence: the rank's part of the answer
@@ -91,6 +106,27 @@ def test_kv_sharded_decode_c_abi_one_rank(variant):
         out_s = comm.decode_kv_sharded(q, k[:, :, lo:].contiguous(), v[:, :, lo:].contiguous(), kv_pos_offset=lo,
                                        seqlen_kv_total=L, **variant)
         assert_bf16_close(out_s.float().cpu().numpy().astype(np.float64), ref_s, "C-ABI suffix shard")
+        # the whole call (decode, NCCL all-gather, combine) captured in a CUDA graph and replayed
+        out_g = torch.empty_like(q)
+        ws = torch.zeros(pb.load().attn_decode_kv_sharded_workspace_bytes(
+            __import__("ctypes").byref(pb._problem(q, k, scale=None, causal=p.causal, window=(-1, -1),
+                                                   alibi_slopes=variant.get("alibi_slopes"), softcap=p.softcap,
+                                                   q_pos_offset=None, kv_pos_offset=0, seqlen_kv_total=L)), 1),
+            dtype=torch.uint8, device="cuda")
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            comm.decode_kv_sharded(q, k, v, kv_pos_offset=0, seqlen_kv_total=L, out=out_g, workspace=ws, **variant)
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            comm.decode_kv_sharded(q, k, v, kv_pos_offset=0, seqlen_kv_total=L, out=out_g, workspace=ws, **variant)
+        out_g.zero_()
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out_g, out)
+        assert int(ws[:256].count_nonzero()) == 0     # tickets reset by every replay
     finally:
         comm.close()
 
