@@ -15,9 +15,16 @@ the KV sequence (strong scaling) and combines the per-rank (m, l, O) triples
 after one NCCL all-gather (paper_2510_08726_b200.dist).
 
 Timing: W warm-up steps, then exactly K steps between barrier +
-synchronize, CUDA events on the launching stream, max over ranks.  Inputs
-are larger than L2 (126 MB) for every timed workload, so no flush is needed.
-nvidia-smi clocks are sampled during the timed region.
+synchronize, CUDA events on the launching stream, max over ranks.  A workload
+whose inputs are smaller than 2 x L2 (the D = 64 configs; a rank's decode KV
+shard at large N) has the L2 flushed between steps (a 252 MB write outside the
+timed events, per-step events); the others are larger than L2.  NVML clocks
+are sampled during every timed region.
+
+At N = 1 the line also carries the other §8(d) configs (C2b ``mha_causal``, C3
+``gqa_window``, C4 ``var_*``), each with clocks and tensor + MUFU rooflines; at
+N > 1 a ``strong_scaling`` object (the fixed C2a problem's (b, h) units
+sharded over the ranks).
 ``--impl reference`` times the fp64 CPU oracle (the reference arm of this
 tier) on a bounded sample of the same workload."""
 from __future__ import annotations
@@ -195,7 +202,8 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_dict(name, args.gpus),
-        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "cpu_model": cpu_model(),
+                         "nproc": os.cpu_count(), "kind": "oracle",
                          "sample": f"1 whole (b, h) head of {name} per step ({S}x{S}, D={D}), fp64 numpy oracle"},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -212,6 +220,52 @@ def config_dict(name, n):
 
 
 # ----------------------------------------------------------------------------- GPU arm
+L2_BYTES = 126 << 20            # B200 L2 (B200_PROFILING.md)
+# The §8(d) configs reported next to the headline in the N = 1 line (each with its own
+# clocks, tensor + MUFU roofline and ncu traffic): C2b, C3 and the C4 variant family.
+EXTRA_WORKLOADS = ("mha_causal", "gqa_window", "var_scaled_dot", "var_alibi_causal", "var_softcap_causal")
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_decode_rate(budget_s: float = 10.0, n_distinct: int = 2, max_groups: int = 4096):
+    """fp64 oracle (as it stands) on whole (b, hkv) groups of config 5 (KV 128K, D = 128, 4 q heads
+    per group): algorithmic K+V GB/s of the groups it finished.  n_distinct groups are generated
+    (the generator is not timed) and cycled until the time budget is spent."""
+    import numpy as np
+
+    import datagen
+    import oracle
+    B, Hq, Hkv, L, D = 16, 32, 8, 131072, 128
+    seed = datagen.config_seed(5)
+    p = oracle.Problem(B, Hq, Hkv, 1, L, D, scale=1.0 / math.sqrt(D), causal=True)
+    rng = np.random.default_rng(5)
+    groups = []
+    for _ in range(n_distinct):
+        b, g = int(rng.integers(B)), int(rng.integers(Hkv))
+        ks = datagen.as_f64(datagen.slab(seed, 2, (B, Hkv, L, D), b, g), "bf16")
+        vs = datagen.as_f64(datagen.slab(seed, 3, (B, Hkv, L, D), b, g), "bf16")
+        qs = [datagen.as_f64(datagen.slab(seed, 1, (B, Hq, 1, D), b, hq), "bf16") for hq in range(g * 4, g * 4 + 4)]
+        groups.append((g, qs, ks, vs))
+    done, t_total = 0, 0.0
+    while done < max_groups and (done == 0 or t_total < budget_s):
+        g, qs, ks, vs = groups[done % n_distinct]
+        t0 = time.perf_counter()
+        for i, hq in enumerate(range(g * 4, g * 4 + 4)):
+            oracle.attention_bh(p, qs[i], ks, vs, hq)
+        t_total += time.perf_counter() - t0
+        done += 1
+    return 2.0 * L * D * 2 * done / t_total / 1e9, done, t_total
+
+
 def main_gpu(args):
     import torch
     import torch.distributed as dist
@@ -238,6 +292,8 @@ def main_gpu(args):
     peaks = load_peaks()
     uuid = str(torch.cuda.get_device_properties(dev).uuid)
     gpu_id = uuid if uuid.startswith("GPU-") else f"GPU-{uuid}"  # NVML form
+    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+    flush_buf = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)   # L2 flush: a write > L2
 
     def barrier():
         if world > 1:
@@ -250,87 +306,113 @@ def main_gpu(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    def timed(fn, steps, warmup, sampler=True):
+    def timed(fn, steps, warmup, sampler=True, flush=False):
+        """ms per step on the device (CUDA events on the launching stream), max over ranks.
+        flush: the L2 is flushed (a 2 x L2 write) between steps, outside the timed events."""
         for _ in range(warmup):
             fn()
         torch.cuda.synchronize()
         barrier()
         torch.cuda.synchronize()
-        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         cs = ClockSampler(gpu_id)
         with (cs if sampler else _Null()):
-            s0.record()
-            for _ in range(steps):
-                fn()
-            s1.record()
-            torch.cuda.synchronize()
+            if flush:
+                evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                       for _ in range(steps)]
+                for e0, e1 in evs:
+                    flush_buf.zero_()
+                    e0.record()
+                    fn()
+                    e1.record()
+                torch.cuda.synchronize()
+                ms = sum(e0.elapsed_time(e1) for e0, e1 in evs) / steps
+            else:
+                s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s0.record()
+                for _ in range(steps):
+                    fn()
+                s1.record()
+                torch.cuda.synchronize()
+                ms = s0.elapsed_time(s1) / steps
         barrier()
-        ms = s0.elapsed_time(s1) / steps
         return max_over_ranks(ms), (cs.summary() if sampler else None)
 
-    # ------------------------------------------------------------- prefill (headline)
-    name = args.workload
-    cid, B, Hq, Hkv, S, D, var = WORKLOADS[name]
-    seed = datagen.config_seed(cid)
-    q = torch.empty(B, Hq, S, D, dtype=torch.bfloat16, device=dev)
-    k = torch.empty(B, Hkv, S, D, dtype=torch.bfloat16, device=dev)
-    v = torch.empty(B, Hkv, S, D, dtype=torch.bfloat16, device=dev)
-    # rank r owns batch rows [rB, (r+1)B) of a global [B*W, ...] tensor (weak scaling)
-    dgd.fill_(q, seed, 1, start=rank * q.numel())
-    dgd.fill_(k, seed, 2, start=rank * k.numel())
-    dgd.fill_(v, seed, 3, start=rank * v.numel())
-    o = torch.empty_like(q)
-    kw = dict(causal=var.get("causal", False), window=var.get("window", (-1, -1)), softcap=var.get("softcap", 0.0))
-    if var.get("alibi"):
-        kw["alibi_slopes"] = torch.tensor(datagen.alibi_slopes(Hq), device=dev)
-    step = lambda: pb.fused_fwd(q, k, v, out=o, **kw)  # noqa: E731
-    step()
-    torch.cuda.synchronize()
-    launches_per_step = pb.last_launch_count()
-    ms, clocks = timed(step, args.steps, args.warmup)
-    flops = 4.0 * D * allowed_pairs(S, var) * B * Hq
-    value = world * flops / (ms * 1e-3) / 1e12
-    achieved = flops / (ms * 1e-3) / 1e12
-    traffic, traffic_decode, traffic_smr = None, None, None
+    traffic_tab = {}
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
-            tr = json.load(open(tpath))
-            traffic = tr.get(f"fwd_{name}")
-            traffic_decode = tr.get(f"decode_b{args.decode_batch}") if world == 1 else None
-            traffic_smr = tr.get("softmax_rows")
+            traffic_tab = json.load(open(tpath))
         except Exception:
-            traffic = None
+            traffic_tab = {}
+
+    # ------------------------------------------------------------- prefill
+    def prefill(name, batch_lo=None, batch_hi=None, steps=None):
+        """One prefill workload: rank r runs its own B-batch shard of a global batch B*W (weak
+        scaling), or batches [batch_lo, batch_hi) of the fixed config (strong scaling)."""
+        cid, B, Hq, Hkv, S, D, var = WORKLOADS[name]
+        seed = datagen.config_seed(cid)
+        if batch_lo is None:
+            b0, nb = rank * B, B
+        else:
+            b0, nb = batch_lo, batch_hi - batch_lo
+        q = torch.empty(nb, Hq, S, D, dtype=torch.bfloat16, device=dev)
+        k = torch.empty(nb, Hkv, S, D, dtype=torch.bfloat16, device=dev)
+        v = torch.empty(nb, Hkv, S, D, dtype=torch.bfloat16, device=dev)
+        dgd.fill_(q, seed, 1, start=b0 * Hq * S * D)
+        dgd.fill_(k, seed, 2, start=b0 * Hkv * S * D)
+        dgd.fill_(v, seed, 3, start=b0 * Hkv * S * D)
+        o = torch.empty_like(q)
+        kw = dict(causal=var.get("causal", False), window=var.get("window", (-1, -1)), softcap=var.get("softcap", 0.0))
+        if var.get("alibi"):
+            kw["alibi_slopes"] = torch.tensor(datagen.alibi_slopes(Hq), device=dev)
+        step = lambda: pb.fused_fwd(q, k, v, out=o, **kw)  # noqa: E731
+        step()
+        torch.cuda.synchronize()
+        launches = pb.last_launch_count()
+        in_bytes = 2 * (q.numel() + k.numel() + v.numel() + o.numel())
+        flush = in_bytes < 2 * L2_BYTES
+        ms, clocks = timed(step, steps or args.steps, args.warmup, flush=flush)
+        flops = 4.0 * D * allowed_pairs(S, var) * nb * Hq
+        achieved = flops / (ms * 1e-3) / 1e12
+        sm_mhz = float((clocks or {}).get("sm_max_mhz") or 1965.0)
+        mufu_ops = allowed_pairs(S, var) * nb * Hq * (2 if var.get("softcap") else 1)
+        mufu_peak = 16.0 * sm_count * sm_mhz * 1e6 / 1e9                      # Gop/s
+        mufu_ach = mufu_ops / (ms * 1e-3) / 1e9
+        tensor = {"bound": "tensor", "achieved": achieved, "peak": peaks["tf"], "unit": "TFLOP/s",
+                  "frac": achieved / peaks["tf"], "traffic": traffic_tab.get(f"fwd_{name}"),
+                  "peak_src": f"{peaks['src']} bf16 burst (MEASURED_PEAKS.json bf16_tflops)",
+                  "kernel": "fwd_tc_persist_kernel" if (D == 128 and var.get("causal") and "window" not in var
+                                                        and not var.get("alibi")) else "fwd_tc_kernel",
+                  "algorithmic_flops_per_launch": flops}
+        # The exponentials (and softcap's tanh) run on the SFU (MUFU): 16 results/clk/SM (measured,
+        # profiles/r1_microbench.md).  At D = 128 a 128x128 tile's exponentials take exactly as long
+        # as its two MMAs; at D = 64 twice as long, so the D = 64 lines are bound by MUFU ("alu").
+        mufu = {"bound": "alu", "achieved": mufu_ach, "peak": mufu_peak, "unit": "Gop/s (MUFU ex2/tanh)",
+                "frac": mufu_ach / mufu_peak, "ops_per_launch": mufu_ops,
+                "peak_src": f"16 MUFU results/clk/SM x {sm_count} SMs x {sm_mhz:.0f} MHz"}
+        if D == 64:
+            roof = dict(mufu, traffic=tensor["traffic"], kernel=tensor["kernel"],
+                        tensor={kk: tensor[kk] for kk in ("achieved", "peak", "unit", "frac")})
+        else:
+            roof = dict(tensor, mufu=mufu)
+        res = {"value": world * flops / (ms * 1e-3) / 1e12 if batch_lo is None else None, "unit": "TFLOP/s",
+               "ms_per_step": ms, "clocks": clocks, "roofline": roof, "gpu_launches_per_step": launches,
+               "config": config_dict(name, world), "flops_per_rank": flops,
+               "l2": "flushed between steps (2 x L2 write, outside the timed events)" if flush
+                     else "inputs larger than L2 (no flush)"}
+        res["config"]["l2"] = res["l2"]
+        return res, (q, k, v, o, kw, flops)
+
+    name = args.workload
+    head, (q, k, v, o, kw, flops) = prefill(name)
     line = {
-        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "metric": METRIC, "value": head["value"], "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded datagen, N(0,1)-like, bf16)",
-        "config": config_dict(name, world), "clocks": clocks,
-        "gpu_launches": launches_per_step * args.steps,
-        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peaks["tf"], "unit": "TFLOP/s",
-                     "frac": achieved / peaks["tf"], "traffic": traffic,
-                     "peak_src": f"{peaks['src']} bf16 burst (MEASURED_PEAKS.json bf16_tflops)",
-                     "kernel": "fwd_tc_kernel (tcgen05 Rolling Update)",
-                     "algorithmic_flops_per_launch": flops},
+        "config": head["config"], "clocks": head["clocks"],
+        "gpu_launches": head["gpu_launches_per_step"] * args.steps,
+        "roofline": head["roofline"],
     }
-    # The exponentials (and softcap's tanh) run on the SFU (MUFU): 16 results/clk/SM (measured,
-    # profiles/r1_microbench.md).  At D = 128 a 128x128 tile's exponentials take exactly as long
-    # as its two MMAs; at D = 64 twice as long, so the D = 64 lines are bound by MUFU ("alu"),
-    # not by the tensor core.  MUFU work = one ex2 per allowed (q, k) pair (+ one tanh with softcap).
-    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
-    sm_mhz = float((clocks or {}).get("sm_max_mhz") or 1965.0)
-    mufu_ops = allowed_pairs(S, var) * B * Hq * (2 if var.get("softcap") else 1)
-    mufu_peak = 16.0 * sm_count * sm_mhz * 1e6 / 1e9                      # Gop/s
-    mufu_ach = mufu_ops / (ms * 1e-3) / 1e9
-    mufu = {"bound": "alu", "achieved": mufu_ach, "peak": mufu_peak, "unit": "Gop/s (MUFU ex2/tanh)",
-            "frac": mufu_ach / mufu_peak, "ops_per_launch": mufu_ops,
-            "peak_src": f"16 MUFU results/clk/SM x {sm_count} SMs x {sm_mhz:.0f} MHz"}
-    if D == 64:
-        tensor = line["roofline"]
-        line["roofline"] = dict(mufu, traffic=traffic, kernel=tensor["kernel"],
-                                tensor={k: tensor[k] for k in ("achieved", "peak", "unit", "frac")})
-    else:
-        line["roofline"]["mufu"] = mufu
 
     # ------------------------------------------------------------- e2e through the public API, host buffers
     if not args.no_e2e:
@@ -343,19 +425,48 @@ def main_gpu(args):
         ms_e2e, _ = timed(e2e_step, e2e_steps, 1, sampler=False)
         line["e2e"] = {"value": world * flops / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOP/s",
                        "h2d_bytes_per_step": 3 * q.numel() * 2, "d2h_bytes_per_step": o.numel() * 2,
-                       "ms_per_step": ms_e2e, "steps": e2e_steps}
+                       "ms_per_step": ms_e2e, "steps": e2e_steps,
+                       "path": "pb.fused_fwd on pinned host tensors (H2D of q, k, v and D2H of o inside the timed "
+                               "region, chunked over two streams)"}
         del hq_, hk_, hv_, ho_
-
     del q, k, v, o
     torch.cuda.empty_cache()
+
+    # ------------------------------------------------------------- the other §8(d) configs (N = 1)
+    if world == 1 and not args.no_workloads:
+        for w in EXTRA_WORKLOADS:
+            if w == name:
+                continue
+            res, tensors = prefill(w)
+            del tensors
+            torch.cuda.empty_cache()
+            line[w] = res
+
+    # ------------------------------------------------------------- strong scaling of C2a (§8(e))
+    if world > 1:
+        cid, B, Hq, Hkv, S, D, var = WORKLOADS[name]
+        if B % world == 0:
+            lo, hi = pdist.shard_range(B, rank, world)
+            res, tensors = prefill(name, lo, hi)
+            del tensors
+            torch.cuda.empty_cache()
+            total = 4.0 * D * allowed_pairs(S, var) * B * Hq
+            line["strong_scaling"] = {
+                "value": total / (res["ms_per_step"] * 1e-3) / 1e12, "unit": "TFLOP/s",
+                "ms_per_step": res["ms_per_step"], "scaling": "strong",
+                "parallelism": f"the fixed {name} problem's {B * Hq} (b, h) units sharded {B // world} batches "
+                               f"x {Hq} heads per rank (shard_range), no collective",
+                "flops_total": total, "clocks": res["clocks"]}
 
     # ------------------------------------------------------------- decode (secondary metric)
     if not args.no_decode:
         Hqd, Hkvd, L, Dd = 32, 8, 131072, 128
         seed5 = datagen.config_seed(5)
         lo, hi = pdist.shard_range(L, rank, world)
+        use_cabi = world > 1 and backend == "nccl"
+        comm = pdist.NcclComm(rank, world) if use_cabi else None
 
-        def run_decode(Bd, steps, warmup):
+        def make_decode_inputs(Bd):
             qd = torch.empty(Bd, Hqd, 1, Dd, dtype=torch.bfloat16, device=dev)
             dgd.fill_(qd, seed5, 1)
             kd = torch.empty(Bd, Hkvd, hi - lo, Dd, dtype=torch.bfloat16, device=dev)
@@ -365,20 +476,29 @@ def main_gpu(args):
                     start = ((b * Hkvd + h) * L + lo) * Dd
                     dgd.fill_(kd[b, h], seed5, 2, start=start)
                     dgd.fill_(vd[b, h], seed5, 3, start=start)
+            return qd, kd, vd
+
+        def run_decode(Bd, steps, warmup):
+            qd, kd, vd = make_decode_inputs(Bd)
             od = torch.empty_like(qd)
-            ws = torch.zeros(pb.workspace_bytes(qd, kd), dtype=torch.uint8, device=dev)  # ticket block must start at 0
+            shard_bytes = 2 * kd.numel() * 2
+            flush = shard_bytes < 2 * L2_BYTES
             if world == 1:
+                ws = torch.zeros(pb.workspace_bytes(qd, kd), dtype=torch.uint8, device=dev)  # tickets start at 0
                 dstep = lambda: pb.splitkv_decode(qd, kd, vd, causal=True, out=od, workspace=ws)  # noqa: E731
+            elif use_cabi:   # the C ABI's one-call path: fused local merge, NCCL all-gather, Eq. 8
+                dstep = lambda: comm.decode_kv_sharded(qd, kd, vd, kv_pos_offset=lo, seqlen_kv_total=L,  # noqa: E731
+                                                       out=od, causal=True)
             else:
                 dstep = lambda: pdist.decode_kv_sharded(qd, kd, vd, kv_pos_offset=lo,  # noqa: E731
                                                         seqlen_kv_total=L, causal=True)
             dstep()
             torch.cuda.synchronize()
             nl = pb.last_launch_count()
-            if world == 1 and not args.no_graph:
+            graphed = (world == 1 or use_cabi) and not args.no_graph
+            if graphed:
                 # A decode step is ~0.1 ms of GPU work at B = 1, less than the Python binding's
-                # per-call host time: capture the step in a CUDA graph (the ABI is capture-safe:
-                # no host sync, tensor maps are kernel parameters) and replay it.
+                # per-call host time: capture the step (NCCL included at N > 1) in a CUDA graph.
                 side = torch.cuda.Stream()
                 side.wait_stream(torch.cuda.current_stream())
                 with torch.cuda.stream(side):
@@ -388,31 +508,26 @@ def main_gpu(args):
                 with torch.cuda.graph(graph):
                     dstep()
                 dstep = graph.replay
-            dms, dclk = timed(dstep, steps, warmup)
+            dms, dclk = timed(dstep, steps, warmup, flush=flush)
             breakdown = None
-            if world > 1:   # local decode, local combine, all-gather, final combine
-                var5 = dict(causal=True)
-                parts = pdist._local_kernels(qd, kd, vd, kv_pos_offset=lo, seqlen_kv_total=L, num_splits=0,
-                                             variant=var5)
-                send = torch.empty(1, Bd, Hqd, Dd + 2, dtype=torch.float32, device=dev)
+            if world > 1:   # local decode (+ fused local merge), all-gather, final combine
+                send = torch.empty(Bd, Hqd, Dd + 2, dtype=torch.float32, device=dev)
                 recv = torch.empty(world, Bd, Hqd, Dd + 2, dtype=torch.float32, device=dev)
+                wsl = torch.zeros(pb.workspace_bytes(qd, kd), dtype=torch.uint8, device=dev)
                 pieces = {
-                    "local_decode": lambda: pdist._local_kernels(qd, kd, vd, kv_pos_offset=lo, seqlen_kv_total=L,
-                                                                 num_splits=0, variant=var5),
-                    "local_combine": lambda: pdist._merge_kernels(parts, pb.Parts.packed(send)),
-                    "all_gather": lambda: dist.all_gather_into_tensor(recv, send),
+                    "local_decode_and_merge": lambda: pb.splitkv_decode(qd, kd, vd, packed=send, workspace=wsl,
+                                                                        kv_pos_offset=lo, seqlen_kv_total=L,
+                                                                        causal=True),
+                    "all_gather": lambda: dist.all_gather_into_tensor(recv.view(world * Bd, Hqd, Dd + 2), send),
                     "final_combine": lambda: pdist._final_kernels(pb.Parts.packed(recv), torch.bfloat16, False),
                 }
-                breakdown = {key: round(timed(fn, steps, 2, sampler=False)[0], 5) for key, fn in pieces.items()}
-                nl = 0   # kernels of one sharded step: local decode + local combine + final combine
-                for key in ("local_decode", "local_combine", "final_combine"):
-                    pieces[key]()
-                    nl += pb.last_launch_count()
-                del parts, send, recv
-            del qd, kd, vd, od, ws
+                breakdown = {key: round(timed(fn, steps, 2, sampler=False, flush=flush)[0], 5)
+                             for key, fn in pieces.items()}
+                del send, recv, wsl
+            del qd, kd, vd, od
             torch.cuda.empty_cache()
             kv_bytes = 2.0 * Bd * Hkvd * L * Dd * 2
-            return kv_bytes, dms, dclk, nl, breakdown
+            return kv_bytes, dms, dclk, nl, breakdown, graphed, flush
 
         def run_decode_bh(Bd, steps, warmup):
             """Communication-free alternative for large B: each rank decodes
@@ -434,37 +549,66 @@ def main_gpu(args):
             return 2.0 * Bd * Hkvd * L * Dd * 2 / (ms * 1e-3) / 1e9, ms
 
         sweep, breakdowns = {}, {}
+        dl, graphed, dflush, dclk_head = 1, False, False, None
         for Bd in sorted(set([1, 4, args.decode_batch])):
-            kv_bytes, dms, dclk, dl, bd = run_decode(Bd, max(args.steps, 20), args.warmup)
+            kv_bytes, dms, dclk, nl, bd, graphed_b, flush_b = run_decode(Bd, max(args.steps, 20), args.warmup)
             sweep[Bd] = {"GB/s": kv_bytes / (dms * 1e-3) / 1e9, "ms_per_step": dms,
                          "frac_of_hbm_peak": kv_bytes / world / (dms * 1e-3) / 1e9 / peaks["hbm"]}
             if bd is not None:
                 breakdowns[str(Bd)] = bd
+            if Bd == args.decode_batch:
+                dl, graphed, dflush, dclk_head = nl, graphed_b, flush_b, dclk
         Bd = args.decode_batch
         gbs, dms = sweep[Bd]["GB/s"], sweep[Bd]["ms_per_step"]
         per_rank = gbs / world
         line["decode"] = {
             "metric": "split-KV decode HBM GB/s (K+V bytes read once / time)", "value": gbs, "unit": "GB/s",
-            "ms_per_step": dms, "scaling": "strong" if world > 1 else None, "clocks": dclk,
+            "ms_per_step": dms, "scaling": "strong" if world > 1 else None, "clocks": dclk_head,
             "config": {"workload": "decode (BASELINE config 5)", "batch": Bd, "heads_q": Hqd, "heads_kv": Hkvd,
                        "kv_len": L, "head_dim": Dd, "causal": True,
-                       "parallelism": f"KV-sequence shard x{world} + NCCL all-gather of (m,l,O)" if world > 1
-                       else "single GPU split-KV", "l2": "KV larger than L2",
-                       "launch": "CUDA graph replay" if world == 1 and not args.no_graph else "eager"},
-            "batch_sweep": {str(b): {k: round(v, 4) for k, v in d.items()} for b, d in sweep.items()},
+                       "parallelism": (f"KV-sequence shard x{world}: fused local merge + NCCL all-gather of (m,l,O) + "
+                                       "Eq. 8 (attn_decode_kv_sharded, one C-ABI call)" if use_cabi else
+                                       f"KV-sequence shard x{world} (torch.distributed all-gather)") if world > 1
+                       else "single GPU split-KV",
+                       "l2": ("flushed between steps (a rank's K/V shard fits in L2)" if dflush
+                              else "KV larger than L2 (no flush)"),
+                       "launch": "CUDA graph replay" if graphed else "eager"},
+            "batch_sweep": {str(b): {kk: round(vv, 4) for kk, vv in d.items()} for b, d in sweep.items()},
             "gpu_launches_per_step": dl,
             "breakdown_ms": breakdowns or None,
             "roofline": {"bound": "hbm", "achieved": per_rank, "peak": peaks["hbm"], "unit": "GB/s",
-                         "frac": per_rank / peaks["hbm"], "traffic": traffic_decode,
+                         "frac": per_rank / peaks["hbm"],
+                         "traffic": traffic_tab.get(f"decode_b{Bd}") if world == 1 else None,
                          "peak_src": f"{peaks['src']} hbm_gbs (copy)", "kernel": "decode_split_kernel (fused Eq. 8 combine)",
                          "algorithmic_bytes_per_launch": 2.0 * Bd * Hkvd * L * Dd * 2 / world},
         }
-
+        # e2e: host q in, host O out through the public API (KV cache resident in HBM, as in serving)
+        if world == 1 and not args.no_e2e:
+            qd, kd, vd = make_decode_inputs(Bd)
+            qh = qd.cpu().pin_memory()
+            fn = lambda: pb.splitkv_decode(qh, kd, vd, causal=True)  # noqa: E731
+            ms_e2e, _ = timed(fn, 10, 3, sampler=False)
+            line["decode"]["e2e"] = {
+                "value": 2.0 * Bd * Hkvd * L * Dd * 2 / (ms_e2e * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms_e2e,
+                "h2d_bytes_per_step": qd.numel() * 2, "d2h_bytes_per_step": qd.numel() * 2,
+                "path": "pb.splitkv_decode(q on pinned host, K/V cache resident on the device) -> O on the host"}
+            del qd, kd, vd, qh
+            torch.cuda.empty_cache()
+        if rank == 0 and world == 1 and not args.no_cpu:
+            rate, groups, secs = oracle_decode_rate(budget_s=args.cpu_budget * 2 / 3)
+            line["decode"]["cpu_baseline"] = {
+                "value": rate, "unit": "GB/s", "cores": blas_threads(), "cpu_model": cpu_model(),
+                "nproc": os.cpu_count(), "kind": "oracle",
+                "sample": f"{groups} (b, hkv) group decodes of config 5 (4 q heads x 131072 keys, D=128; 2 distinct "
+                          f"groups cycled) in {secs:.1f} s, fp64 numpy oracle (oracle.attention_bh); GB/s = their "
+                          "K+V bf16 bytes / time"}
         if world > 1 and args.decode_batch % world == 0:
             gbs_bh, ms_bh = run_decode_bh(args.decode_batch, max(args.steps, 20), args.warmup)
             line["decode"]["bh_sharded"] = {
                 "GB/s": gbs_bh, "ms_per_step": ms_bh, "scaling": "strong",
                 "parallelism": f"(b, hkv) sharding: {args.decode_batch // world} sequences per rank, no collective"}
+        if comm is not None:
+            comm.close()
 
     # ------------------------------------------------------------- NEXT-4: Fig. 2 reduction chain (softmax rows)
     if not args.no_softmax:
@@ -480,18 +624,21 @@ def main_gpu(args):
         sgbs = sbytes / (sms * 1e-3) / 1e9
         line["softmax_rows"] = {
             "metric": "Fig. 2 chain (row max, row sum, softmax) HBM GB/s (x read + y write)", "value": world * sgbs,
-            "unit": "GB/s", "ms_per_step": sms, "scaling": "weak" if world > 1 else None,
-            "config": {"workload": "softmax rows (NEXT-4)", "rows": rows, "cols": cols, "dtype": "bf16"},
+            "unit": "GB/s", "ms_per_step": sms, "scaling": "weak" if world > 1 else None, "clocks": sclk,
+            "config": {"workload": "softmax rows (NEXT-4)", "rows": rows, "cols": cols, "dtype": "bf16",
+                       "l2": "inputs larger than L2 (no flush)"},
             "roofline": {"bound": "hbm", "achieved": sgbs, "peak": peaks["hbm"], "unit": "GB/s",
-                         "frac": sgbs / peaks["hbm"], "traffic": traffic_smr, "kernel": "softmax_rows16_kernel",
-                         "algorithmic_bytes_per_launch": sbytes},
+                         "frac": sgbs / peaks["hbm"], "traffic": traffic_tab.get("softmax_rows"),
+                         "kernel": "softmax_rows16_kernel", "algorithmic_bytes_per_launch": sbytes},
         }
         del xs, ys
 
     # ------------------------------------------------------------- CPU baseline (oracle), rank 0, N = 1
     if rank == 0 and world == 1 and not args.no_cpu:
+        cid, B, Hq, Hkv, S, D, var = WORKLOADS[name]
         rate, heads, secs = oracle_sample_rate(name, budget_s=args.cpu_budget)
-        line["cpu_baseline"] = {"value": rate, "unit": "TFLOP/s", "cores": blas_threads(), "kind": "oracle",
+        line["cpu_baseline"] = {"value": rate, "unit": "TFLOP/s", "cores": blas_threads(), "cpu_model": cpu_model(),
+                                "nproc": os.cpu_count(), "kind": "oracle",
                                 "sample": f"{heads} whole (b,h) heads of {name} ({S}x{S}, D={D}) in {secs:.1f} s, "
                                           "fp64 numpy oracle (oracle.attention_bh)"}
     if rank == 0:
@@ -520,6 +667,7 @@ def main():
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-softmax", action="store_true")
+    ap.add_argument("--no-workloads", action="store_true", help="skip the other §8(d) prefill configs (N = 1)")
     ap.add_argument("--no-graph", action="store_true", help="decode: eager launches instead of a CUDA graph")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()
