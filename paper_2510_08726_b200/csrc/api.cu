@@ -218,8 +218,9 @@ attn_status attn_fused_fwd_splitkv(const attn_problem* prob, attn_tensor q, attn
     a.v = vp;
     a.lse = lse;
     if ((st = make_map(&a.tm_q, q, p.batch, p.heads_q, p.seqlen_q, p.head_dim, 64, 128, true, a.f16)) != ATTN_OK) return st;
-    if ((st = make_map(&a.tm_k, k, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, 128, true, a.f16)) != ATTN_OK) return st;
-    if ((st = make_map(&a.tm_v, v, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, 128, true, a.f16)) != ATTN_OK) return st;
+    const int bn = attn::fwd_kv_tile_keys(p.head_dim);
+    if ((st = make_map(&a.tm_k, k, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, bn, true, a.f16)) != ATTN_OK) return st;
+    if ((st = make_map(&a.tm_v, v, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, bn, true, a.f16)) != ATTN_OK) return st;
     // (the prefill kernels prefetch tm_o even when they write fp32 partials: always a valid map)
     if ((st = make_map(&a.tm_o, o, p.batch, p.heads_q, p.seqlen_q, p.head_dim, 64, 128, true, a.f16)) != ATTN_OK) return st;
     if (num_splits <= 1)
@@ -305,8 +306,9 @@ attn_status attn_fused_fwd_partial(const attn_problem* prob, attn_tensor q, attn
   a.lse = lse;
   a.s.o_part = o_part;
   if ((st = make_map(&a.tm_q, q, p.batch, p.heads_q, p.seqlen_q, p.head_dim, 64, 128, true, a.f16)) != ATTN_OK) return st;
-  if ((st = make_map(&a.tm_k, k, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, 128, true, a.f16)) != ATTN_OK) return st;
-  if ((st = make_map(&a.tm_v, v, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, 128, true, a.f16)) != ATTN_OK) return st;
+  const int bn = attn::fwd_kv_tile_keys(p.head_dim);
+  if ((st = make_map(&a.tm_k, k, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, bn, true, a.f16)) != ATTN_OK) return st;
+  if ((st = make_map(&a.tm_v, v, p.batch, p.heads_kv, p.seqlen_kv, p.head_dim, 64, bn, true, a.f16)) != ATTN_OK) return st;
   a.tm_o = a.tm_q;   // never stored through (prefetched only)
   int launches = 0;
   st = cuda_status(attn::launch_fwd_tc(a, reinterpret_cast<cudaStream_t>(stream), &launches), "fwd_tc launch");

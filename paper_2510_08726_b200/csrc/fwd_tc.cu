@@ -48,7 +48,6 @@ constexpr int kThreads = (kSoftmaxWarps + 3) * 32;
 constexpr float kTau = 8.0f;                      // lazy-repair threshold (log2 units), reading R9
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr uint32_t kBarTok0 = 3, kBarTok1 = 4;   // named barriers of the exp token
 constexpr uint32_t kBarP0 = 5;                    // 5 / 6: "P_t ready" (softmax threads of tile t + MMA warp)
 constexpr uint32_t kBarS0 = 9;                    // 9 / 10: "S_t loaded into registers" (P in smem only)
 // Causal block order: heaviest-first over a group of (head, batch) slices whose K/V fit in
@@ -61,15 +60,15 @@ constexpr bool kTraceBuild = false;
 #endif
 
 #define WAIT_SM(bar, par) mbar_wait(bar, par)        // softmax waits for S: try_wait (HW sleep)
-#define WAIT_LM(bar, par) mbar_wait_spin(bar, par)   // loader / MMA thread waits: poll
+#define WAIT_LM(bar, par) mbar_wait_spin(bar, par)   // loader / MMA thread waits: poll (try_wait: equal)
 
 #ifdef ATTN_TRACE
 // Debug-only timeline of one CTA: clock() per (event, step), kept in shared
 // memory while the kernel runs (so tracing adds no global-memory traffic
 // before the mbarrier releases) and copied to g_trace at the end.
 // 32-bit clock() samples (the host unwraps differences modulo 2^32).
-constexpr int kTrEv = 26, kTrSteps = 24;
-__device__ long long g_trace[kTrEv][40];
+constexpr int kTrEv = 32, kTrSteps = 16;
+__device__ long long g_trace[kTrEv][kTrSteps];
 __device__ __forceinline__ bool trace_cta() { return blockIdx.x == 5 && blockIdx.y == 3 && blockIdx.z == 2; }
 #define TRACE(ev, step)                                                          \
   do {                                                                           \
@@ -87,17 +86,27 @@ __device__ __forceinline__ bool trace_cta() { return blockIdx.x == 5 && blockIdx
 // ALiBi (without softcap) is folded into the QK contraction at both head dims (kExt).
 template <int D>
 __host__ __device__ constexpr int nt_of() { return D == 128 ? 2 : 1; }
+// KV tile width: D = 64 uses 64-key tiles so that a CTA needs 128 TMEM columns (S 64 + O 64) and
+// FOUR 128-row CTAs (16 softmax warps) share an SM: the D = 64 kernel is bound by the latency of
+// each CTA's softmax <-> tensor-core chain, not by MUFU throughput, so more independent CTAs per
+// SM is what raises the exponential rate.  Same-box A/B (r2, vs 128-key tiles with 2 CTAs/SM):
+// scaled-dot +12 %, causal +18 %, softcap-causal +14 %, ALiBi-causal +12 %, ALiBi +11 %.
+template <int D>
+__host__ __device__ constexpr int bn_of() { return D == 64 ? 64 : 128; }
 template <int D, bool kAlibi>
-__host__ __device__ constexpr bool alibi_mma() { return kAlibi; }
+__host__ __device__ constexpr bool alibi_mma() { return kAlibi && !(D == 128 && kTraceBuild); }   // (trace: no smem left)
 
 template <int D, bool kExt = false, int NT = 2>
 struct Cfg {
   static constexpr int kBoxes = D / 64;           // 64-column (128 B) swizzle atoms per row
   static constexpr int kQTileBytes = BM * D * 2;
-  static constexpr int kKVTileBytes = BN * D * 2;
-  static constexpr bool kPS = D == 128;          // P in shared memory (else in TMEM, aliasing S)
-  static constexpr int kPTileBytes = kPS ? BM * BN * 2 : 0;
-  static constexpr int kStages = D == 128 ? 3 : 5;
+  static constexpr int BNk = bn_of<D>();
+  static constexpr int kKVTileBytes = BNk * D * 2;
+  // P in shared memory at D = 128 (else in TMEM, aliasing S: at D = 64 P in shared memory with a
+  // 3-slot ring measured equal, r2)
+  static constexpr bool kPS = D == 128;
+  static constexpr int kPTileBytes = kPS ? BM * BNk * 2 : 0;
+  static constexpr int kStages = D == 128 ? 3 : 4;   // D = 64: 4 x 8 KiB slots (4 CTAs per SM)
   // Load-group barriers (ring).  The producer can be at most kStages/2 groups
   // ahead of the issuer's wait, so kStages/2 + 1 barriers never alias a phase.
   static constexpr int kPairBars = kStages / 2 + 1;
@@ -136,6 +145,7 @@ __device__ __forceinline__ void row_bounds(const Shape& s, const VariantParams& 
   jhi = (int)max(hi, -1LL);
 }
 
+template <int BNt = BN>
 __device__ __forceinline__ Range tile_range(const Shape& s, const VariantParams& v, int i0) {
   Range r{0, 0, 0, -1, 0, -1};
   if (i0 >= s.Sq) return r;
@@ -143,24 +153,46 @@ __device__ __forceinline__ Range tile_range(const Shape& s, const VariantParams&
   row_bounds(s, v, v.q_off + i0, r.jlo_first, r.jhi_first);
   row_bounds(s, v, v.q_off + il, r.jlo_last, r.jhi_last);
   if (r.jlo_first <= r.jhi_last) {
-    r.lo = r.jlo_first / BN;
-    r.hi = r.jhi_last / BN + 1;
+    r.lo = r.jlo_first / BNt;
+    r.hi = r.jhi_last / BNt + 1;
   }
   return r;
 }
 
 __device__ __forceinline__ bool active(const Range& r, int j) { return j >= r.lo && j < r.hi; }
 
+// MUFU offload: pair e (of the 16 pairs of a 32-column chunk) takes the FMA-pipe exp2
+// (ex2_poly2) for kPolyPairs evenly spread pairs, MUFU ex2.approx for the rest.  Same-box A/B
+// (r2, pairs of 16 on the polynomial): persistent causal D = 128 4/16 +3.6 %; D = 64 (4 CTAs/SM)
+// 2/16: scaled-dot +3 %, softcap +4 %, ALiBi equal (ALiBi keeps MUFU only: 4/16 cost it 4-8 %);
+// grid kernel D = 128 4/16 -2 %, 6/16 -8 % (there the MUFU is not the binding unit: the exp phase
+// is paced by synchronisation).
+constexpr int kPolyGrid128 = 0, kPolyGrid64 = 2, kPolyPersist = 4;
+template <int kPolyPairs>
+__device__ __forceinline__ constexpr bool poly_pair(int e) {
+  return kPolyPairs > 0 && ((e * kPolyPairs) % 16) + kPolyPairs >= 16;
+}
+template <int kPolyPairs>
+__device__ __forceinline__ void exp2_pair(float a0, float a1, float& p0, float& p1, int e) {
+  if (poly_pair<kPolyPairs>(e)) {
+    ex2_poly2(a0, a1, p0, p1);
+  } else {
+    p0 = ex2_approx(a0);
+    p1 = ex2_approx(a1);
+  }
+}
+
 // ALiBi-in-MMA class of (query tile starting at row i0, KV tile j): +1 if every key is at or
 // before every query of the tile (bias = -slope (qpos - kpos) = slope*c + a row constant:
 // A_ext(+s)), -1 if every key is at or after every query (A_ext(-s)), 0 mixed (A_ext(+s) and
 // a per-element fix-up).  The issuer and the softmax threads classify identically.
+template <int BNt = BN>
 __device__ __forceinline__ int ext_class(const Shape& s, const VariantParams& v, int i0, int j) {
   // Causal: every ALLOWED key of any tile is at or before its query, so the linear form holds
   // for the allowed elements of a diagonal tile too (the rest are masked to -inf).
   if (v.causal) return 1;
   const long long qf = v.q_off + i0, ql = v.q_off + min(i0 + BM, s.Sq) - 1;
-  const long long k0 = v.kv_off + (long long)j * BN, k1 = k0 + BN - 1;
+  const long long k0 = v.kv_off + (long long)j * BNt, k1 = k0 + BNt - 1;
   if (k1 <= qf) return 1;
   if (k0 >= ql) return -1;
   return 0;
@@ -252,31 +284,34 @@ __device__ __forceinline__ float score_tile_ext_mixed(float (&x)[N], const Varia
   });
 }
 
-template <int NT>
+template <int NT, int BNt = BN>
 struct Roles {   // warp roles of fwd_tc_kernel
   static constexpr int kSoftmaxWarps = NT * kTileThreads / 32;
   static constexpr int kWarpLoad = kSoftmaxWarps, kWarpMma = kSoftmaxWarps + 1;
   static constexpr int kWarpAlloc = NT == 2 ? kSoftmaxWarps + 2 : kWarpMma;   // NT = 1: the MMA warp allocates
   static constexpr int kThreads = (NT == 2 ? kSoftmaxWarps + 3 : kSoftmaxWarps + 2) * 32;
-  static constexpr int kMinBlocks = NT == 2 ? 1 : 2;
-  static constexpr int kTmemCols = NT == 2 ? 512 : 256;
-  static constexpr uint32_t kOBase = NT == 2 ? 256 : 128;   // TMEM column of O_0 (S_t at t * 128)
+  // NT = 1: 2 CTAs per SM at 128-key tiles (256 TMEM columns each), 4 at 64-key tiles (128 each)
+  static constexpr int kMinBlocks = NT == 2 ? 1 : (BNt == 64 ? 4 : 2);
+  static constexpr int kTmemCols = NT == 2 ? 512 : (BNt == 64 ? 128 : 256);
+  static constexpr uint32_t kOBase = NT == 2 ? 256 : BNt;   // TMEM column of O_0 (S_t at t * 128)
 };
 
 template <int D, bool kAlibi, bool kSoftcap, bool kF16, int NT>
-__global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
+__global__ void __launch_bounds__(Roles<NT, bn_of<D>()>::kThreads, Roles<NT, bn_of<D>()>::kMinBlocks)
     fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o, const Shape s,
                   const VariantParams v, float* __restrict__ lse) {
   constexpr bool kExt = alibi_mma<D, kAlibi && !kSoftcap>();   // softcap: the bias follows the tanh
   constexpr bool kChunkMask = D == 128;   // chunk-classified masking (measured: + at D = 128, - at D = 64)
   using C = Cfg<D, kExt, NT>;
-  using Ro = Roles<NT>;
+  using Ro = Roles<NT, C::BNk>;
+  constexpr int BN = C::BNk;   // KV tile width of this kernel (shadows the file constant)
   constexpr int kSoftmaxWarps = Ro::kSoftmaxWarps, kWarpLoad = Ro::kWarpLoad, kWarpMma = Ro::kWarpMma;
   constexpr int kWarpAlloc = Ro::kWarpAlloc;
   constexpr bool kPSmem = C::kPS;
   constexpr bool kF32x2 = D == 128;   // packed FFMA2 / FADD2 (measured: +1.5-2 % at D = 128, -4 % at D = 64)
-  constexpr bool kToken = NT == 2;    // the two tiles' exp phases alternate (+2 %)
+  // (r1 alternated the two tiles' exp phases through a named-barrier token; r2 same-box A/B
+  // without it: MHA +2.2 %, GQA window +1 %)
   constexpr bool kPlain = !kAlibi && !kSoftcap;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // The 128-byte swizzle needs 1024-byte aligned tiles; dynamic shared memory
@@ -296,7 +331,7 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
   uint64_t* o_done = p_ready + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 #ifdef ATTN_TRACE
-  uint32_t* s_trace = reinterpret_cast<uint32_t*>(smem + C::kSmemQ + C::kSmemKV + C::kExt2Bytes + C::kXchgBytes + 256);
+  uint32_t* s_trace = reinterpret_cast<uint32_t*>(smem + C::kSmemQ + C::kSmemKV + C::kExt2Bytes + 256);
   if (trace_cta())
     for (int i = threadIdx.x; i < kTrEv * kTrSteps; i += blockDim.x) s_trace[i] = 0;
 #endif
@@ -323,9 +358,10 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
   const int b = s.kv_splits > 1 ? zb % s.B : zb;              // input batch index
   const int hkv = hq / (s.Hq / s.Hkv);                       // R6: contiguous GQA groups
   const int row0 = qblk * NT * BM;
-  Range rng0 = tile_range(s, v, row0), rng1 = NT == 2 ? tile_range(s, v, row0 + BM) : Range{0, 0, 0, -1, 0, -1};
+  Range rng0 = tile_range<BN>(s, v, row0), rng1 = NT == 2 ? tile_range<BN>(s, v, row0 + BM) : Range{0, 0, 0, -1, 0, -1};
   if (s.kv_splits > 1) {   // this CTA's KV split: a contiguous run of whole tiles
-    const int t_lo = (zb / s.B) * s.kv_split_tiles, t_hi = t_lo + s.kv_split_tiles;
+    // (kv_split_tiles counts 128-key tiles, the host's unit)
+    const int t_lo = (zb / s.B) * s.kv_split_tiles * (128 / BN), t_hi = t_lo + s.kv_split_tiles * (128 / BN);
     for (Range* r : {&rng0, &rng1}) {
       r->lo = max(r->lo, t_lo);
       r->hi = min(r->hi, t_hi);
@@ -501,7 +537,7 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
         }
         if constexpr (kExt) {
           if (ext_on) {
-            const int cls = ext_class(s, v, row0 + t * BM, J(j));
+            const int cls = ext_class<BN>(s, v, row0 + t * BM, J(j));
             const uint32_t sa = smem_u32(sExt + (cls < 0 ? 256 : 0));
             mma_ss_warp(tS[t], smem_desc_nosw(sa, 128, 0), smem_desc_nosw(smem_u32(sExt + 512), 0, 128), idesc_qk, 1u);
           }
@@ -629,15 +665,8 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
 
     // Ping-pong: the exp phases of the two tiles alternate in KV-tile order
     // (token passed through named barriers 3/4).
-    if (kToken && t == 1 && uhi > ulo) named_bar_arrive(kBarTok0, 2 * kTileThreads);
     for (int j = ulo; j < uhi; ++j) {
-      if (!active(R, j)) {   // keep the token moving through tiles this tile skips
-        if (!kToken) continue;
-        named_bar_sync(t == 0 ? kBarTok0 : kBarTok1, 2 * kTileThreads);
-        if (t == 0) named_bar_arrive(kBarTok1, 2 * kTileThreads);
-        else if (j + 1 < uhi) named_bar_arrive(kBarTok0, 2 * kTileThreads);
-        continue;
-      }
+      if (!active(R, j)) continue;
       const int it = j - R.lo;
       if (tid_t == 0) TRACE(4 + 4 * t, j);
       WAIT_SM(&s_full[t], it & 1);
@@ -658,6 +687,7 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
 #pragma unroll
         for (int c = 0; c < BN; ++c) x[c] = u2f(u[c]);
       }
+      if (tid_t == 0) TRACE(26 + 3 * t, j);   // S in registers
       // Fig. 19 max_local (+ score_mod, mask) -> max_global
       const int jt = J(j);   // the KV tile of step j
       const bool need_mask = !(jt * BN >= R.jlo_last && (jt + 1) * BN - 1 <= R.jhi_first);
@@ -668,7 +698,7 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
       float mt;
       if (kExt && ext_on) {
         // ALiBi in the contraction: S already holds q.k + (+-s) c (see ext_class)
-        const int cls = ext_class(s, v, row0 + t * BM, jt);
+        const int cls = ext_class<BN>(s, v, row0 + t * BM, jt);
         if (cls != 0) {   // bias = row constant: the plain path with an offset
           e_mul = v.scale_log2;
           e_off = (cls > 0 ? nslope2 : -nslope2) * dq0;
@@ -695,6 +725,7 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
       if (need_o) alpha = ex2_approx(m_ref - m_run);   // repair term h = exp(r - r') (Fig. 18d)
       if (move) m_ref = m_run;
       l *= alpha;                                       // xsum = h(xsum) + ...
+      if (tid_t == 0) TRACE(27 + 3 * t, j);   // max and repair factor done
       // exp(x - m), local sum, P -> bf16 into TMEM (aliasing S)
       const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
       if constexpr (kPSmem) {
@@ -705,9 +736,12 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
           tc_fence_after();
         }
       }
-      if (kToken) named_bar_sync(t == 0 ? kBarTok0 : kBarTok1, 2 * kTileThreads);   // acquire the exp token
+      if (tid_t == 0) TRACE(28 + 3 * t, j);   // PV_t(j-1) done
+      float e_add = e_off - m_use;
+#ifdef ATTN_TRACE
+      asm volatile("" : "+f"(e_add));   // trace builds: the exponentials are not hoisted above this point
+#endif
       if (tid_t == 0) TRACE(6 + 4 * t, j);
-      const float e_add = e_off - m_use;
       float sum0 = 0.f, sum1 = 0.f;
 #pragma unroll
       for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -721,7 +755,8 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
             a0 = fmaf(x[c0 + 2 * e], e_mul, e_add);
             a1 = fmaf(x[c0 + 2 * e + 1], e_mul, e_add);
           }
-          const float p0 = ex2_approx(a0), p1 = ex2_approx(a1);
+          float p0, p1;
+          exp2_pair<D == 128 ? kPolyGrid128 : (kAlibi ? 0 : kPolyGrid64)>(a0, a1, p0, p1, e);
           if constexpr (kF32x2) {
             add2_acc(sum0, sum1, p0, p1);
           } else {
@@ -742,10 +777,6 @@ __global__ void __launch_bounds__(Roles<NT>::kThreads, Roles<NT>::kMinBlocks)
         } else {
           tmem_st16(tP + c0 / 2, pk);
         }
-      }
-      if (kToken) {                                         // release the token
-        if (t == 0) named_bar_arrive(kBarTok1, 2 * kTileThreads);
-        else if (j + 1 < uhi) named_bar_arrive(kBarTok0, 2 * kTileThreads);
       }
       const float sum = sum0 + sum1;
       if (tid_t == 0) TRACE(7 + 4 * t, j);
@@ -1184,7 +1215,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int e = 0; e < 16; ++e) {
             float a0, a1;   // exponent argument (log2 units), packed FFMA2
             fma2_bc(a0, a1, x[c0 + 2 * e], x[c0 + 2 * e + 1], kPlain ? v.scale_log2 : 1.f, e_add);
-            const float p0 = ex2_approx(a0), p1 = ex2_approx(a1);
+            float p0, p1;
+            exp2_pair<kPolyPersist>(a0, a1, p0, p1, e);
             add2_acc(sum0, sum1, p0, p1);
             pk[e] = pack2<kF16>(p0, p1);
           }
@@ -1353,6 +1385,8 @@ extern "C" __attribute__((visibility("default"))) int attn_debug_trace(long long
   return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(g_trace));
 }
 #endif
+
+int fwd_kv_tile_keys(int D) { return D == 64 ? bn_of<64>() : bn_of<128>(); }
 
 cudaError_t launch_fwd_tc(const FwdTcArgs& a, cudaStream_t stream, int* launches) {
   cudaError_t e = a.f16 ? (a.s.D == 128 ? launch_d<128, true>(a, stream) : launch_d<64, true>(a, stream))

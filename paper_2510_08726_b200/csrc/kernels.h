@@ -59,6 +59,7 @@ struct FwdTcArgs {
   CUtensorMap tm_q, tm_k, tm_v, tm_o;
 };
 cudaError_t launch_fwd_tc(const FwdTcArgs& a, cudaStream_t stream, int* launches);
+int fwd_kv_tile_keys(int D);   // KV tile width (keys) of the prefill kernel: the K/V TMA box rows
 
 // ------------------------------------------------------------ fp32 SIMT forward
 struct FwdSimtArgs {

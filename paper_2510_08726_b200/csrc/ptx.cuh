@@ -310,6 +310,32 @@ __device__ __forceinline__ void add2_acc(float& s0, float& s1, float a0, float a
   f32x2_split(d, s0, s1);
 }
 
+// 2^a0, 2^a1 on the FMA/ALU pipes (MUFU offload, FA4-style): a = k + f with k = round(a)
+// (the 1.5*2^23 + 127 add leaves k + 127 in the low mantissa bits), 2^f by a degree-3
+// minimax polynomial on f in [-1/2, 1/2] (relative error 7.5e-5, below the 2^-9 half-ulp
+// of the bf16 / 2^-11 of the fp16 P it feeds), times 2^k built in the exponent field.
+// a is clamped to >= -127, where 2^k's bit pattern is +0.0: masked (-inf) inputs give an
+// exact 0 like ex2.approx; otherwise a < -126 underflows to <= 2^-126 (true value
+// < 2^-126).  Packed f32x2 arithmetic: 9 FMA-pipe / 4 ALU instructions per pair.
+__device__ __forceinline__ void ex2_poly2(float a0, float a1, float& r0, float& r1) {
+  constexpr float kMagic = 12582912.f + 127.f;   // 1.5 * 2^23 + 127
+  const float c0 = fmaxf(a0, -127.f), c1 = fmaxf(a1, -127.f);
+  unsigned long long t, u, f, p;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(f32x2(c0, c1)), "l"(f32x2(kMagic, kMagic)));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(u) : "l"(t), "l"(f32x2(kMagic, kMagic)));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(f) : "l"(f32x2(c0, c1)), "l"(u));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(f), "l"(f32x2(0.05517109f, 0.05517109f)),
+      "l"(f32x2(0.24261115f, 0.24261115f)));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(p), "l"(f), "l"(f32x2(0.6932611f, 0.6932611f)));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(p), "l"(f), "l"(f32x2(0.99992806f, 0.99992806f)));
+  float t0, t1;
+  f32x2_split(t, t0, t1);
+  const unsigned long long sc = f32x2(__uint_as_float(__float_as_uint(t0) << 23), __uint_as_float(__float_as_uint(t1) << 23));
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(p), "l"(sc));
+  f32x2_split(r, r0, r1);
+}
+
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

@@ -19,11 +19,24 @@ causal = len(sys.argv) > 1 and sys.argv[1] == "causal"
 for _ in range(3):
     o = pb.fused_fwd(q, k, v, causal=causal)
 torch.cuda.synchronize()
-tr = np.zeros((26, 40), dtype=np.int64)
+tr = np.zeros((32, 16), dtype=np.int64)
 ctypes.CDLL(lib_path).attn_debug_trace(tr.ctypes.data_as(ctypes.c_void_p))
 t0 = tr[3, 0]
 names = {12: "mma:V ready", 13: "mma:P0 seen", 15: "mma:K+1 ready", 14: "mma:P1 seen", 0: "mma:PV0 iss", 1: "mma:QK0+1 iss", 2: "mma:PV1 iss", 4: "sm0:wait S", 5: "sm0:S ready",
-         6: "sm0:token", 7: "sm0:P done", 8: "sm1:wait S", 9: "sm1:S ready", 10: "sm1:token", 11: "sm1:P done", 16: "w4 exp end", 17: "w5 exp end", 18: "w6 exp end", 19: "w7 exp end", 20: "w4 arrive", 21: "w5 arrive", 22: "w6 arrive", 23: "w7 arrive", 24: "ld:K issue", 25: "ld:V issue"}
+         6: "sm0:exp start", 7: "sm0:P done", 8: "sm1:wait S", 9: "sm1:S ready", 10: "sm1:exp start", 11: "sm1:P done", 16: "w4 exp end", 17: "w5 exp end", 18: "w6 exp end", 19: "w7 exp end", 20: "w4 arrive", 21: "w5 arrive", 22: "w6 arrive", 23: "w7 arrive", 26: "sm0:S regs", 27: "sm0:max", 28: "sm0:o_done", 29: "sm1:S regs", 30: "sm1:max", 31: "sm1:o_done"}
 print("step " + " ".join(f"{names[e]:>13s}" for e in names))
-for j in range(min(33, S // 128 + 1)):
+for j in range(min(16, S // 128 + 1)):
     print(f"{j:4d} " + " ".join(f"{((tr[e, j] - t0) & 0xffffffff) if tr[e, j] else 0:13d}" for e in names))
+# sorted event timeline of a few steady-state steps
+print()
+evs = []
+for j in range(8, 11):
+    for e, nm in names.items():
+        if tr[e, j]:
+            evs.append((int((tr[e, j] - t0) & 0xffffffff), j, nm))
+evs.sort()
+base = evs[0][0]
+prev = base
+for t, j, nm in evs:
+    print(f"{t - base:7d} (+{t - prev:5d})  step {j:2d}  {nm}")
+    prev = t
