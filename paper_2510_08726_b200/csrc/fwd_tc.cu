@@ -801,10 +801,13 @@ __global__ void __launch_bounds__(Roles<NT, bn_of<D>()>::kThreads, Roles<NT, bn_
       tmem_st_wait();
       l += sum;
 #ifdef ATTN_STRICT_WAITS
-      // Sanitizer build: observe every o_done phase (the production kernel only
-      // waits when it rescales O; it can never fall two phases behind).
+      // Checking build: the TMEM-aliased-P path (D = 64) waits on o_done only when it rescales O.
+      // Skipping the other phases is safe because S_t(j) is produced by the QK MMA the issuer
+      // enqueued AFTER PV_t(j-1), and the tcgen05.commit behind s_full tracks every earlier MMA of
+      // that thread: s_full(j) complete => PV_t(j-1) complete.  Assert it (trap if the phase is not
+      // complete), which also observes every phase for compute-sanitizer's synccheck.
       if (!kPSmem && it > 0 && !__any_sync(0xffffffffu, need_o)) {
-        mbar_wait(&o_done[t], (it - 1) & 1);
+        if (!mbar_test_wait(&o_done[t], (it - 1) & 1)) __trap();
         tc_fence_after();
       }
 #endif
