@@ -13,6 +13,12 @@
 #ifndef ATTN_WATCHDOG_SPINS
 #define ATTN_WATCHDOG_SPINS (1u << 26)
 #endif
+// The watchdog traps a wait that never completes (a hung kernel becomes a launch error).  Its
+// printf (block, thread, barrier) is a debug option: the vprintf call inside every wait loop
+// makes the hot loops respect the call ABI, which costs registers (spills) in the prefill kernels.
+#ifndef ATTN_WATCHDOG_PRINTF
+#define ATTN_WATCHDOG_PRINTF 0
+#endif
 
 namespace attn {
 
@@ -62,8 +68,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t spins = 0;
   while (!mbar_try_wait(bar, parity)) {
     if (++spins > ATTN_WATCHDOG_SPINS) {
+#if ATTN_WATCHDOG_PRINTF
       printf("attn watchdog: block (%d,%d,%d) thread %d stuck on mbarrier %p parity %u\n", blockIdx.x,
              blockIdx.y, blockIdx.z, threadIdx.x, bar, parity);
+#endif
       __trap();
     }
   }
@@ -85,8 +93,10 @@ __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
   uint32_t spins = 0;
   while (!mbar_test_wait(bar, parity)) {
     if (++spins > 16u * ATTN_WATCHDOG_SPINS) {
+#if ATTN_WATCHDOG_PRINTF
       printf("attn watchdog (spin): block (%d,%d,%d) thread %d stuck on mbarrier %p parity %u\n", blockIdx.x,
              blockIdx.y, blockIdx.z, threadIdx.x, bar, parity);
+#endif
       __trap();
     }
   }
