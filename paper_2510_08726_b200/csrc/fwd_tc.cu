@@ -164,10 +164,10 @@ __device__ __forceinline__ bool active(const Range& r, int j) { return j >= r.lo
 // MUFU offload: pair e (of the 16 pairs of a 32-column chunk) takes the FMA-pipe exp2
 // (ex2_poly2) for kPolyPairs evenly spread pairs, MUFU ex2.approx for the rest.  Same-box A/B
 // (r2, pairs of 16 on the polynomial): persistent causal D = 128 4/16 +3.6 %; D = 64 (4 CTAs/SM)
-// 2/16: scaled-dot +3 %, softcap +4 %, ALiBi equal (ALiBi keeps MUFU only: 4/16 cost it 4-8 %);
-// grid kernel D = 128 4/16 -2 %, 6/16 -8 % (there the MUFU is not the binding unit: the exp phase
-// is paced by synchronisation).
-constexpr int kPolyGrid128 = 0, kPolyGrid64 = 2, kPolyPersist = 4;
+// 2/16: scaled-dot +3 %, softcap +4 %; grid kernel D = 128 2/16 +1 % (MHA), 4/16 -1 … -2 %,
+// 6/16 -8 % (the MUFU is not the binding unit there: the exp phase is paced by synchronisation,
+// DESIGN.md §4.1); ALiBi kernels keep MUFU only (2/16 -2 %, 4/16 -4 … -8 %).
+constexpr int kPolyGrid128 = 2, kPolyGrid64 = 2, kPolyPersist = 4;   // (ALiBi kernels: 0)
 template <int kPolyPairs>
 __device__ __forceinline__ constexpr bool poly_pair(int e) {
   return kPolyPairs > 0 && ((e * kPolyPairs) % 16) + kPolyPairs >= 16;
@@ -756,7 +756,7 @@ __global__ void __launch_bounds__(Roles<NT, bn_of<D>()>::kThreads, Roles<NT, bn_
             a1 = fmaf(x[c0 + 2 * e + 1], e_mul, e_add);
           }
           float p0, p1;
-          exp2_pair<D == 128 ? kPolyGrid128 : (kAlibi ? 0 : kPolyGrid64)>(a0, a1, p0, p1, e);
+          exp2_pair<kAlibi ? 0 : (D == 128 ? kPolyGrid128 : kPolyGrid64)>(a0, a1, p0, p1, e);
           if constexpr (kF32x2) {
             add2_acc(sum0, sum1, p0, p1);
           } else {
