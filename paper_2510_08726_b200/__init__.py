@@ -29,9 +29,10 @@ _DT = {torch.bfloat16: _ffi.ATTN_BF16, torch.float32: _ffi.ATTN_FP32, torch.floa
 def _as_tensor(t: Optional[torch.Tensor]) -> AttnTensor:
     if t is None:
         return AttnTensor(None, 0, 0, 0)
-    if t.dim() != 4 or t.stride(3) != 1:
+    st = t.stride()
+    if len(st) != 4 or st[3] != 1:
         raise ValueError("expected a [B, H, S, D] tensor with a contiguous last dimension")
-    return AttnTensor(t.data_ptr(), t.stride(0), t.stride(1), t.stride(2))
+    return AttnTensor(t.data_ptr(), st[0], st[1], st[2])
 
 
 def _stream(stream) -> ctypes.c_void_p:
@@ -42,25 +43,27 @@ def _stream(stream) -> ctypes.c_void_p:
 def _check_io(q, k, v, out=None, lse=None, lse_shape=None):
     """Shape / dtype / device checks the C ABI cannot make (it sees only pointers and
     strides, not allocation sizes): a mismatch here would be an out-of-bounds device
-    access, so it raises ValueError before anything is launched."""
-    for name, t in (("q", q), ("k", k), ("v", v)):
-        if t.dim() != 4:
-            raise ValueError(f"{name} must be a [B, H, S, D] tensor (got {tuple(t.shape)})")
-    if v.shape != k.shape:
-        raise ValueError(f"v {tuple(v.shape)} must have k's shape {tuple(k.shape)}")
-    if k.shape[0] != q.shape[0] or k.shape[3] != q.shape[3]:
+    access, so it raises ValueError before anything is launched.  (Kept cheap: it runs on
+    every call, and small calls are launch-bound.)"""
+    qs, ks, vs = q.shape, k.shape, v.shape
+    if len(qs) != 4 or len(ks) != 4:
+        raise ValueError(f"q, k must be [B, H, S, D] tensors (got {tuple(qs)}, {tuple(ks)})")
+    if vs != ks:
+        raise ValueError(f"v {tuple(vs)} must have k's shape {tuple(ks)}")
+    if ks[0] != qs[0] or ks[3] != qs[3]:
         raise ValueError("q and k disagree on batch or head_dim")
-    if k.shape[1] < 1 or q.shape[1] % k.shape[1] != 0:
-        raise ValueError(f"heads_q ({q.shape[1]}) must be a multiple of heads_kv ({k.shape[1]})")
-    for name, t in (("k", k), ("v", v)) + ((("out", out),) if out is not None else ()):
-        if t.dtype != q.dtype:
-            raise ValueError(f"{name} dtype {t.dtype} differs from q's {q.dtype}")
-        if t.device != q.device:
-            raise ValueError(f"{name} is on {t.device}, q on {q.device}")
-    if out is not None and out.shape != q.shape:
-        raise ValueError(f"out {tuple(out.shape)} must have q's shape {tuple(q.shape)}")
+    if ks[1] < 1 or qs[1] % ks[1] != 0:
+        raise ValueError(f"heads_q ({qs[1]}) must be a multiple of heads_kv ({ks[1]})")
+    dt, dev = q.dtype, q.get_device()
+    if k.dtype is not dt or v.dtype is not dt or (out is not None and out.dtype is not dt):
+        raise ValueError(f"k / v / out dtype ({k.dtype}, {v.dtype}, {None if out is None else out.dtype}) "
+                         f"differs from q's {dt}")
+    if k.get_device() != dev or v.get_device() != dev or (out is not None and out.get_device() != dev):
+        raise ValueError(f"k / v / out must be on q's device {q.device}")
+    if out is not None and out.shape != qs:
+        raise ValueError(f"out {tuple(out.shape)} must have q's shape {tuple(qs)}")
     if lse is not None:
-        if lse.dtype != torch.float32 or not lse.is_contiguous() or lse.device != q.device:
+        if lse.dtype is not torch.float32 or lse.get_device() != dev or not lse.is_contiguous():
             raise ValueError("lse must be a contiguous float32 tensor on q's device")
         if tuple(lse.shape) != tuple(lse_shape):
             raise ValueError(f"lse must have shape {tuple(lse_shape)} (got {tuple(lse.shape)})")

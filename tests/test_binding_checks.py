@@ -21,9 +21,9 @@ def qkv(B=1, Hq=4, Hkv=2, Sq=64, Skv=64, D=128):
 @pytest.mark.parametrize("bad,match", [
     (dict(v=t(1, 2, 63, 128)), "v .* must have k's shape"),
     (dict(k=t(1, 2, 64, 128, dtype=torch.float32), v=t(1, 2, 64, 128, dtype=torch.float32)), "dtype"),
-    (dict(v=t(1, 2, 64, 128, dtype=torch.float16)), "v dtype"),
+    (dict(v=t(1, 2, 64, 128, dtype=torch.float16)), "dtype"),
     (dict(out=t(1, 4, 32, 128)), "out .* must have q's shape"),
-    (dict(out=t(1, 4, 64, 128, dtype=torch.float16)), "out dtype"),
+    (dict(out=t(1, 4, 64, 128, dtype=torch.float16)), "dtype"),
     (dict(lse=torch.empty(1, 4, 32, device=M)), "lse must have shape"),
     (dict(lse=torch.empty(1, 4, 64, device=M, dtype=torch.float64)), "float32"),
     (dict(k=t(1, 3, 64, 128), v=t(1, 3, 64, 128)), "multiple of heads_kv"),
