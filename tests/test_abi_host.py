@@ -178,3 +178,30 @@ def test_prefill_split_heuristic_is_host_only(lib):
     assert lib.attn_fused_fwd_default_splits(ctypes.byref(wide), 148) == 1      # 128 units: < 4 per unit
     f32 = _prob(batch=1, heads_q=2, heads_kv=2, seqlen_q=16, seqlen_kv=4096, dtype=_ffi.ATTN_FP32)
     assert lib.attn_fused_fwd_default_splits(ctypes.byref(f32), 148) == 1
+
+
+def test_partial_and_packed_argument_errors(lib):
+    """attn_fused_fwd_partial (fp32 CP partial) and attn_splitkv_decode_packed (the KV-sharded
+    decode's send triple): host-side argument checks, no device access."""
+    p = _prob()
+    assert lib.attn_fused_fwd_partial(ctypes.byref(p), _t(), _t(), _t(), None, FAKE, None) == \
+        _ffi.ATTN_ERR_INVALID_ARGUMENT                      # o_part required
+    assert lib.attn_fused_fwd_partial(ctypes.byref(p), _t(), _t(), _t(), FAKE + 4, FAKE, None) == \
+        _ffi.ATTN_ERR_ALIGNMENT                             # o_part 16-byte aligned
+    f32 = _prob(dtype=_ffi.ATTN_FP32)
+    assert lib.attn_fused_fwd_partial(ctypes.byref(f32), _t(), _t(), _t(), FAKE, FAKE, None) == \
+        _ffi.ATTN_ERR_UNSUPPORTED                           # bf16 / fp16 inputs only
+    d = _prob(seqlen_q=1)
+    assert lib.attn_splitkv_decode_packed(ctypes.byref(d), _t(), _t(), _t(), 0, None, 0, None, None) == \
+        _ffi.ATTN_ERR_INVALID_ARGUMENT                      # packed required
+    assert lib.attn_splitkv_decode_packed(ctypes.byref(d), _t(), _t(), _t(), 0, None, 0, FAKE, None) == \
+        _ffi.ATTN_ERR_WORKSPACE_TOO_SMALL                   # ticket workspace required
+    m = _prob(seqlen_q=2)
+    assert lib.attn_splitkv_decode_packed(ctypes.byref(m), _t(), _t(), _t(), 0, None, 0, FAKE, None) == \
+        _ffi.ATTN_ERR_UNSUPPORTED                           # one query per (b, hq)
+
+
+def test_repair_counter_hook_is_host_only(lib):
+    """attn_debug_repair_counters only records a pointer (thread-local) for later calls."""
+    lib.attn_debug_repair_counters(FAKE)
+    lib.attn_debug_repair_counters(None)
