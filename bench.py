@@ -387,9 +387,12 @@ def main_gpu(args):
         # The exponentials (and softcap's tanh) run on the SFU (MUFU): 16 results/clk/SM (measured,
         # profiles/r1_microbench.md).  At D = 128 a 128x128 tile's exponentials take exactly as long
         # as its two MMAs; at D = 64 twice as long, so the D = 64 lines are bound by MUFU ("alu").
+        sm_now = float((clocks or {}).get("sm_mhz") or sm_mhz)
         mufu = {"bound": "alu", "achieved": mufu_ach, "peak": mufu_peak, "unit": "Gop/s (MUFU ex2/tanh)",
                 "frac": mufu_ach / mufu_peak, "ops_per_launch": mufu_ops,
-                "peak_src": f"16 MUFU results/clk/SM x {sm_count} SMs x {sm_mhz:.0f} MHz"}
+                "peak_src": f"16 MUFU results/clk/SM x {sm_count} SMs x {sm_mhz:.0f} MHz (max SM clock)",
+                # the same bound at the SM clock sampled during this run (the SFU rate scales with it)
+                "frac_at_sampled_clock": mufu_ach / (16.0 * sm_count * sm_now * 1e6 / 1e9)}
         if D == 64:
             roof = dict(mufu, traffic=tensor["traffic"], kernel=tensor["kernel"],
                         tensor={kk: tensor[kk] for kk in ("achieved", "peak", "unit", "frac")})
@@ -437,6 +440,9 @@ def main_gpu(args):
         for w in EXTRA_WORKLOADS:
             if w == name:
                 continue
+            # the board settles below its boost clock after seconds of full-power compute (no NVML
+            # reason); an idle pause before each config keeps them comparable
+            time.sleep(args.cooldown)
             res, tensors = prefill(w)
             del tensors
             torch.cuda.empty_cache()
@@ -460,6 +466,7 @@ def main_gpu(args):
 
     # ------------------------------------------------------------- decode (secondary metric)
     if not args.no_decode:
+        time.sleep(args.cooldown)
         Hqd, Hkvd, L, Dd = 32, 8, 131072, 128
         seed5 = datagen.config_seed(5)
         lo, hi = pdist.shard_range(L, rank, world)
@@ -670,6 +677,7 @@ def main():
     ap.add_argument("--no-workloads", action="store_true", help="skip the other §8(d) prefill configs (N = 1)")
     ap.add_argument("--no-graph", action="store_true", help="decode: eager launches instead of a CUDA graph")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--cooldown", type=float, default=2.0, help="idle seconds before each secondary config")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
