@@ -163,11 +163,12 @@ __device__ __forceinline__ bool active(const Range& r, int j) { return j >= r.lo
 
 // MUFU offload: pair e (of the 16 pairs of a 32-column chunk) takes the FMA-pipe exp2
 // (ex2_poly2) for kPolyPairs evenly spread pairs, MUFU ex2.approx for the rest.  Same-box A/B
-// (r2, pairs of 16 on the polynomial): persistent causal D = 128 4/16 +3.6 %; D = 64 (4 CTAs/SM)
-// 2/16: scaled-dot +3 %, softcap +4 %; grid kernel D = 128 2/16 +1 % (MHA), 4/16 -1 … -2 %,
+// (r2, pairs of 16 on the polynomial): persistent causal D = 128 2/16 +4 %, 4/16 +1 %, 6/16 -4 %
+// (vs none); D = 64 (4 CTAs/SM) 2/16: scaled-dot +3 %, softcap +4 %; grid kernel D = 128 2/16
+// +1 % (MHA), 4/16 -1 … -2 %,
 // 6/16 -8 % (the MUFU is not the binding unit there: the exp phase is paced by synchronisation,
 // DESIGN.md §4.1); ALiBi kernels keep MUFU only (2/16 -2 %, 4/16 -4 … -8 %).
-constexpr int kPolyGrid128 = 2, kPolyGrid64 = 2, kPolyPersist = 4;   // (ALiBi kernels: 0)
+constexpr int kPolyGrid128 = 2, kPolyGrid64 = 2, kPolyPersist = 2;   // (ALiBi kernels: 0)
 template <int kPolyPairs>
 __device__ __forceinline__ constexpr bool poly_pair(int e) {
   return kPolyPairs > 0 && ((e * kPolyPairs) % 16) + kPolyPairs >= 16;
