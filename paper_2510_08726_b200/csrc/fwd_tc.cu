@@ -9,23 +9,24 @@
 // O / l after the loop (Fig. 9 reverse_compute_at(norm)).
 //
 // B200 mapping:
-//   CTA = 2 query tiles of BM = 128 rows of one (b, hq) -> 256 rows; 352 threads.
-//   warps 0-3   : softmax/correction/epilogue for query tile 0 (thread = row)
-//   warps 4-7   : same for query tile 1
-//   warp 8      : TMA producer (Q once; K_j / V_j through a ring of kStages slots)
-//   warp 9      : tcgen05.mma issuer (warp-wide, one elected lane issues)
-//   warp 10     : TMEM allocator (512 columns)
-//   The producer and MMA warps get the HIGHEST warp ids on purpose: the warp
-//   arbiter is highest-id-first, so they are never starved by the softmax warps.
-//   TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512) (fp32 columns).
-//   P_t (bf16/fp16) goes to shared memory in the UMMA K-major layout (default,
-//   ATTN_P_SMEM=1): S_t is free as soon as its softmax threads hold it in
-//   registers, so the issue order per KV step j is PV0(j), QK0(j+2), PV1(j),
-//   QK1(j+2) and S_t(j+1) is computed while the softmax of step j runs; K
-//   runs two tiles ahead of V in the 3-slot ring.  (ATTN_P_SMEM=0: P aliases
-//   the first 64 columns of S_t in TMEM and feeds a TS MMA; order PV0(j),
-//   QK0(j+1), PV1(j), QK1(j+1) -- the tile's chain softmax -> PV -> QK is
-//   serial; measured 3 % slower.)
+//   D = 128: CTA = 2 query tiles of BM = 128 rows of one (b, hq) -> 256 rows; 352 threads.
+//     warps 0-3   : softmax/correction/epilogue for query tile 0 (thread = row)
+//     warps 4-7   : same for query tile 1
+//     warp 8      : TMA producer (Q once; K_j / V_j through a 3-slot ring of 128-key tiles)
+//     warp 9      : tcgen05.mma issuer (warp-wide, one elected lane issues)
+//     warp 10     : TMEM allocator (512 columns)
+//     The producer and MMA warps get the HIGHEST warp ids on purpose: the warp
+//     arbiter is highest-id-first, so they are never starved by the softmax warps.
+//     TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512) (fp32 columns).
+//     P_t (bf16/fp16) goes to shared memory in the UMMA K-major layout: S_t is free as soon as
+//     its softmax threads hold it in registers, so the issue order per KV step j is PV0(j),
+//     QK0(j+2), PV1(j), QK1(j+2) and S_t(j+1) is computed while the softmax of step j runs; K
+//     runs two tiles ahead of V in the ring.  (P aliasing S in TMEM with a TS MMA serialises
+//     softmax -> PV -> QK per tile: measured 3 % (r1, with the exp token) to 10 % (r2) slower.)
+//     Pure-causal problems run the persistent variant (fwd_tc_persist_kernel) of this layout.
+//   D = 64: CTA = ONE 128-row query tile, 64-key KV tiles, 192 threads (4 softmax warps, TMA
+//     producer, MMA issuer + TMEM allocator), TMEM S [0,64) (P aliasing it) + O [64,128): four
+//     CTAs per SM.
 //   Repair is lazy (reading R9): the reference max r' only moves when the
 //   running max exceeds it by more than kTau (log2 units); exact because h
 //   tag-updates to any reference (Eq. 6).
@@ -79,10 +80,12 @@ __device__ __forceinline__ bool trace_cta() { return blockIdx.x == 5 && blockIdx
 #endif
 
 // Shipped configuration per head dim (the measured alternatives are listed there):
-//   D = 128: NT = 2 query tiles per CTA (one CTA per SM, the tiles' exp phases alternate through a
-//            named-barrier token), P in shared memory (PV = SS MMA, S released early), 3-slot
-//            K/V ring, packed f32x2 exponent FMA / row sum, chunk-classified masks.
-//   D = 64 : NT = 1 (two 128-row CTAs per SM), P aliasing S in TMEM (PV = TS MMA), 5-slot ring.
+//   D = 128: NT = 2 query tiles per CTA (one CTA per SM, the two tiles' exponentials overlap),
+//            P in shared memory (PV = SS MMA, S released early), 3-slot K/V ring of 128-key
+//            tiles, packed f32x2 exponent FMA / row sum, chunk-classified masks.
+//   D = 64 : NT = 1 (four 128-row CTAs per SM), 64-key tiles, P aliasing S in TMEM (PV = TS
+//            MMA), 4-slot ring.
+// Both: 2 of every 16 exponential pairs on the FMA pipe (ex2_poly2) except with ALiBi.
 // ALiBi (without softcap) is folded into the QK contraction at both head dims (kExt).
 template <int D>
 __host__ __device__ constexpr int nt_of() { return D == 128 ? 2 : 1; }
@@ -664,8 +667,6 @@ __global__ void __launch_bounds__(Roles<NT, bn_of<D>()>::kThreads, Roles<NT, bn_
     float m_ref = -INFINITY;  // stale reference max (log2 units), R9
     float l = 0.f;            // running denominator over this thread's columns (un-rounded fp32 p, R10)
 
-    // Ping-pong: the exp phases of the two tiles alternate in KV-tile order
-    // (token passed through named barriers 3/4).
     for (int j = ulo; j < uhi; ++j) {
       if (!active(R, j)) continue;
       const int it = j - R.lo;
