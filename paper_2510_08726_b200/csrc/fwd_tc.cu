@@ -60,7 +60,7 @@ constexpr bool kTraceBuild = true;    // the timeline trace instruments the non-
 constexpr bool kTraceBuild = false;
 #endif
 
-#define WAIT_SM(bar, par) mbar_wait(bar, par)        // softmax waits for S: try_wait (HW sleep)
+#define WAIT_SM(bar, par) mbar_wait(bar, par)        // softmax waits: try_wait (HW sleep; test_wait polling: equal / -2.5 % at D = 64)
 #define WAIT_LM(bar, par) mbar_wait_spin(bar, par)   // loader / MMA thread waits: poll (try_wait: equal)
 
 #ifdef ATTN_TRACE
@@ -222,14 +222,17 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
 // where the chunk branches cost registers in the MUFU-bound kernels.)
 template <bool kMask, bool kChunked, int N, class XF>
 __device__ __forceinline__ float row_max_pass(float (&x)[N], int rel_lo, int rel_hi, XF xf) {
-  float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};   // independent chains for ILP
+  constexpr int kCh = 4;
+  float mx[kCh];   // independent chains for ILP
+#pragma unroll
+  for (int q = 0; q < kCh; ++q) mx[q] = -INFINITY;
   if constexpr (!kChunked) {
 #pragma unroll
     for (int c = 0; c < N; ++c) {
       float xv = xf(x[c], c);
       if constexpr (kMask) xv = (c >= rel_lo && c <= rel_hi) ? xv : -INFINITY;
       x[c] = xv;
-      mx[c & 3] = fmaxf(mx[c & 3], xv);
+      mx[c % kCh] = fmaxf(mx[c % kCh], xv);
     }
   } else {
 #pragma unroll
@@ -242,7 +245,7 @@ __device__ __forceinline__ float row_max_pass(float (&x)[N], int rel_lo, int rel
         const int c = q * 32 + e;
         const float xv = xf(x[c], c);
         x[c] = xv;
-        mx[c & 3] = fmaxf(mx[c & 3], xv);
+        mx[c % kCh] = fmaxf(mx[c % kCh], xv);
       }
     } else {
 #pragma unroll
@@ -250,12 +253,16 @@ __device__ __forceinline__ float row_max_pass(float (&x)[N], int rel_lo, int rel
         const int c = q * 32 + e;
         const float xv = (c >= rel_lo && c <= rel_hi) ? xf(x[c], c) : -INFINITY;
         x[c] = xv;
-        mx[c & 3] = fmaxf(mx[c & 3], xv);
+        mx[c % kCh] = fmaxf(mx[c % kCh], xv);
       }
     }
   }
   }
-  return fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+#pragma unroll
+  for (int w = kCh / 2; w > 0; w /= 2)
+#pragma unroll
+    for (int q = 0; q < w; ++q) mx[q] = fmaxf(mx[q], mx[q + w]);
+  return mx[0];
 }
 
 // score_mod + mask of one S row (BN raw fp32 dots in `x`), in place, into the
@@ -286,6 +293,36 @@ __device__ __forceinline__ float score_tile_ext_mixed(float (&x)[N], const Varia
   return row_max_pass<kMask, false>(x, rel_lo, rel_hi, [&](float xv, int c) {
     return fmaf(nslope2, fmaxf(dq0, 2.f * (float)c - dq0), xv * v.scale_log2);
   });
+}
+
+// One accumulator's whole K loop as ONE batched issue (ptx.cuh mma_*_x4/x8: a single elect.sync
+// for the batch, so the issuing warp keeps the tensor rate and leaves its sub-partition's issue
+// slots to the softmax warps).  SW128 K-major A / B: k-step kk starts (kk >> 2) atoms of
+// kAtomA / kAtomB bytes and (kk & 3) * 32 bytes into the tile; V (MN-major B of PV) advances
+// 2048 bytes (16 keys) per k-step.  Descriptor start addresses are in 16-byte units.
+template <int NK>
+__device__ __forceinline__ void mma_ss_kloop(uint32_t d, uint64_t da, uint32_t atom_a, uint64_t db, uint32_t atom_b,
+                                             bool b_mn16, uint32_t idesc, uint32_t acc) {
+  uint64_t a[NK], b[NK];
+#pragma unroll
+  for (int kk = 0; kk < NK; ++kk) {
+    a[kk] = da + (uint64_t)(((kk >> 2) * atom_a + (kk & 3) * 32) >> 4);
+    b[kk] = db + (uint64_t)((b_mn16 ? kk * 2048 : (kk >> 2) * atom_b + (kk & 3) * 32) >> 4);
+  }
+  if constexpr (NK == 8) mma_ss_x8(d, a, b, idesc, acc);
+  else mma_ss_x4(d, a, b, idesc, acc);
+}
+template <int NK>
+__device__ __forceinline__ void mma_ts_kloop(uint32_t d, uint32_t ta, uint64_t db, uint32_t idesc, uint32_t acc) {
+  uint32_t a[NK];
+  uint64_t b[NK];
+#pragma unroll
+  for (int kk = 0; kk < NK; ++kk) {
+    a[kk] = ta + kk * 8;                              // 16 keys of 16-bit P = 8 TMEM columns
+    b[kk] = db + (uint64_t)((kk * 2048) >> 4);
+  }
+  if constexpr (NK == 8) mma_ts_x8(d, a, b, idesc, acc);
+  else mma_ts_x4(d, a, b, idesc, acc);
 }
 
 template <int NT, int BNt = BN>
@@ -475,6 +512,7 @@ __global__ void __launch_bounds__(Roles<NT, bn_of<D>()>::kThreads, Roles<NT, bn_
         int it = 0;
         auto load = [&](bool is_k, int jj) {
           WAIT_LM(&kv_empty[it % C::kStages], ((it / C::kStages) & 1) ^ 1);
+          TRACE(24 + (is_k ? 0 : 1), jj);   // slot free: the load is issued now (trace builds)
           uint64_t* bar = &kv_full[it % C::kStages];
           mbar_arrive_expect_tx(bar, C::kKVTileBytes);
           uint8_t* dst = sKV + (it % C::kStages) * C::kKVTileBytes;
@@ -532,12 +570,17 @@ __global__ void __launch_bounds__(Roles<NT, bn_of<D>()>::kThreads, Roles<NT, bn_
       auto qk = [&](int t, int it, int j) {   // S_t = Q_t K_j^T (+ s*c, ALiBi in the contraction)
         const uint32_t sq = smem_u32(sQ + t * C::kQTileBytes);
         const uint32_t sk = smem_u32(sKV + (it % C::kStages) * C::kKVTileBytes);
+        if constexpr (kPSmem) {   // D = 128 grid kernel: per-MMA issue (batched: MHA -1 %, ALiBi -5 %, r2 A/B)
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t ka = (kk >> 2) * (BM * 128) + (kk & 3) * 32;
-          const uint32_t kb = (kk >> 2) * (BN * 128) + (kk & 3) * 32;
-          mma_ss_warp(tS[t], smem_desc_sw128(sq + ka, 16, 1024), smem_desc_sw128(sk + kb, 16, 1024), idesc_qk,
-                 kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t ka = (kk >> 2) * (BM * 128) + (kk & 3) * 32;
+            const uint32_t kb = (kk >> 2) * (BN * 128) + (kk & 3) * 32;
+            mma_ss_warp(tS[t], smem_desc_sw128(sq + ka, 16, 1024), smem_desc_sw128(sk + kb, 16, 1024), idesc_qk,
+                        kk > 0 ? 1u : 0u);
+          }
+        } else {
+          mma_ss_kloop<D / 16>(tS[t], smem_desc_sw128(sq, 16, 1024), BM * 128, smem_desc_sw128(sk, 16, 1024), BN * 128,
+                               false, idesc_qk, 0u);
         }
         if constexpr (kExt) {
           if (ext_on) {
@@ -553,10 +596,7 @@ __global__ void __launch_bounds__(Roles<NT, bn_of<D>()>::kThreads, Roles<NT, bn_
         tc_fence_after();
         if (lane == 0) TRACE(13 + t, it / 2);
         const uint32_t sv = smem_u32(sKV + (it % C::kStages) * C::kKVTileBytes);
-#pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk)
-          mma_ts_warp(tO[t], tS[t] + kk * 8, smem_desc_sw128(sv + kk * 2048, BN * 128, 1024), idesc_pv,
-                 (acc || kk > 0) ? 1u : 0u);
+        mma_ts_kloop<BN / 16>(tO[t], tS[t], smem_desc_sw128(sv, BN * 128, 1024), idesc_pv, acc ? 1u : 0u);
         mma_commit_warp(&o_done[t]);
       };
 
@@ -674,6 +714,7 @@ __global__ void __launch_bounds__(Roles<NT, bn_of<D>()>::kThreads, Roles<NT, bn_
       WAIT_SM(&s_full[t], it & 1);
       tc_fence_after();
       if (tid_t == 0) TRACE(5 + 4 * t, j);
+      if (t == 0 && tid_t == 32) TRACE(20, j);   // warp quarter 1: S ready
       float x[BN];
       {
         uint32_t u[BN];
@@ -690,6 +731,7 @@ __global__ void __launch_bounds__(Roles<NT, bn_of<D>()>::kThreads, Roles<NT, bn_
         for (int c = 0; c < BN; ++c) x[c] = u2f(u[c]);
       }
       if (tid_t == 0) TRACE(26 + 3 * t, j);   // S in registers
+      if (t == 0 && tid_t == 32) TRACE(21, j);
       // Fig. 19 max_local (+ score_mod, mask) -> max_global
       const int jt = J(j);   // the KV tile of step j
       const bool need_mask = !(jt * BN >= R.jlo_last && (jt + 1) * BN - 1 <= R.jhi_first);
@@ -728,13 +770,14 @@ __global__ void __launch_bounds__(Roles<NT, bn_of<D>()>::kThreads, Roles<NT, bn_
       if (move) m_ref = m_run;
       l *= alpha;                                       // xsum = h(xsum) + ...
       if (tid_t == 0) TRACE(27 + 3 * t, j);   // max and repair factor done
+      if (t == 0 && tid_t == 32) TRACE(22, j);
       // exp(x - m), local sum, P -> bf16 into TMEM (aliasing S)
       const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
       if constexpr (kPSmem) {
         // PV_t(j-1) must be complete before P_t(j) overwrites sP_t
         // (the rare O rescale stays after the exponentials, where the S registers are dead)
         if (it > 0) {
-          mbar_wait(&o_done[t], (it - 1) & 1);
+          WAIT_SM(&o_done[t], (it - 1) & 1);
           tc_fence_after();
         }
       }
@@ -744,6 +787,7 @@ __global__ void __launch_bounds__(Roles<NT, bn_of<D>()>::kThreads, Roles<NT, bn_
       asm volatile("" : "+f"(e_add));   // trace builds: the exponentials are not hoisted above this point
 #endif
       if (tid_t == 0) TRACE(6 + 4 * t, j);
+      if (t == 0 && tid_t == 32) TRACE(23, j);
       float sum0 = 0.f, sum1 = 0.f;
 #pragma unroll
       for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -815,7 +859,7 @@ __global__ void __launch_bounds__(Roles<NT, bn_of<D>()>::kThreads, Roles<NT, bn_
 #endif
       if constexpr (kPSmem) fence_proxy_async_smem();   // generic-proxy P stores -> tensor core reads
       tc_fence_before();
-      if (t == 0 && lane == 0 && wt < 4) TRACE(20 + wq, j);
+
       named_bar_arrive(kBarP0 + t, kTileThreads + 32);   // P_t(j) in TMEM / smem -> MMA issuer
     }
 
@@ -1089,13 +1133,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         qk_any[t] = true;
         const uint32_t sq = smem_u32(sQ + t * kTile);
         const uint32_t sk = smem_u32(sKV + (i % kStages) * kKV);
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t ka = (kk >> 2) * (BM * 128) + (kk & 3) * 32;
-          const uint32_t kb = (kk >> 2) * (BN * 128) + (kk & 3) * 32;
-          mma_ss_warp(tS[t], smem_desc_sw128(sq + ka, 16, 1024), smem_desc_sw128(sk + kb, 16, 1024), idesc_qk,
-                      kk > 0 ? 1u : 0u);
-        }
+        mma_ss_kloop<D / 16>(tS[t], smem_desc_sw128(sq, 16, 1024), BM * 128, smem_desc_sw128(sk, 16, 1024), BN * 128,
+                             false, idesc_qk, 0u);
         mma_commit_warp(&s_full[t]);
       };
       auto pv = [&](int t, int i, bool acc) {   // O_t += P_t V (P from this unit's P region)
@@ -1103,12 +1142,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t sp = smem_u32(sP + t * kTile);
         const uint32_t sv = smem_u32(sKV + (i % kStages) * kKV);
-#pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk) {
-          const uint32_t ka = (kk >> 2) * (BM * 128) + (kk & 3) * 32;
-          mma_ss_warp(tO[t], smem_desc_sw128(sp + ka, 16, 1024), smem_desc_sw128(sv + kk * 2048, BN * 128, 1024),
-                      idesc_pv, (acc || kk > 0) ? 1u : 0u);
-        }
+        mma_ss_kloop<BN / 16>(tO[t], smem_desc_sw128(sp, 16, 1024), BM * 128, smem_desc_sw128(sv, BN * 128, 1024), 0,
+                              true, idesc_pv, acc ? 1u : 0u);
         mma_commit_warp(&o_done[t]);
       };
       // Q(k) must have landed even for a unit without KV work: pv_done #k may only
@@ -1174,7 +1209,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint8_t* sP = region((k + 1) & 1) + t * kTile;
       float m_ref = -INFINITY, l = 0.f;
       for (int j = R.lo; j < R.hi; ++j) {
-        mbar_wait(&s_full[t], n_s & 1);
+        WAIT_SM(&s_full[t], n_s & 1);
         ++n_s;
         tc_fence_after();
         float x[BN];
@@ -1209,7 +1244,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
         const float e_add = -m_use;
         if (n_pv > 0) {                 // PV_t of the previous step (maybe of the previous unit) is done
-          mbar_wait(&o_done[t], (n_pv - 1) & 1);
+          WAIT_SM(&o_done[t], (n_pv - 1) & 1);
           tc_fence_after();
         }
         float sum0 = 0.f, sum1 = 0.f;

@@ -222,6 +222,70 @@ __device__ __forceinline__ void mma_ts_warp(uint32_t d_tmem, uint32_t a_tmem, ui
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// A whole K loop of one accumulator (4 or 8 MMAs) from ONE asm block with ONE elect.sync.
+// Per-MMA elect.sync makes ptxas wrap every UTCHMMA in its own elect/branch loop; with another
+// warp on the sub-partition that issue stream ran at ~140 cycles per M128 N128 K16 MMA (64 is
+// the tensor rate) and stole ~20 % of the sub-partition's issue slots.  The batched form issues
+// at the tensor rate and costs the neighbour warps ~3 % (tools/issue_block.cu, r2).
+// `acc` = 0: the first MMA overwrites D (enable-input-d false), the rest accumulate.
+#define ATTN_MMA_BATCH_HEAD                                                                   \
+  "{\n .reg .pred p, q, e;\n .reg .b32 r;\n setp.ne.b32 p, %2, 0;\n setp.eq.b32 q, %2, %2;\n" \
+  " elect.sync r|e, 0xffffffff;\n"
+__device__ __forceinline__ void mma_ss_x8(uint32_t d, const uint64_t (&a)[8], const uint64_t (&b)[8], uint32_t idesc,
+                                          uint32_t acc) {
+  asm volatile(ATTN_MMA_BATCH_HEAD
+               " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %3, %11, %1, p;\n"
+               " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %4, %12, %1, q;\n"
+               " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %5, %13, %1, q;\n"
+               " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %6, %14, %1, q;\n"
+               " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %7, %15, %1, q;\n"
+               " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %8, %16, %1, q;\n"
+               " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %9, %17, %1, q;\n"
+               " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %10, %18, %1, q;\n}\n" ::"r"(d),
+               "r"(idesc), "r"(acc), "l"(a[0]), "l"(a[1]), "l"(a[2]), "l"(a[3]), "l"(a[4]), "l"(a[5]), "l"(a[6]),
+               "l"(a[7]), "l"(b[0]), "l"(b[1]), "l"(b[2]), "l"(b[3]), "l"(b[4]), "l"(b[5]), "l"(b[6]), "l"(b[7])
+               : "memory");
+}
+__device__ __forceinline__ void mma_ss_x4(uint32_t d, const uint64_t (&a)[4], const uint64_t (&b)[4], uint32_t idesc,
+                                          uint32_t acc) {
+  asm volatile(ATTN_MMA_BATCH_HEAD
+               " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %3, %7, %1, p;\n"
+               " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %4, %8, %1, q;\n"
+               " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %5, %9, %1, q;\n"
+               " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %6, %10, %1, q;\n}\n" ::"r"(d),
+               "r"(idesc), "r"(acc), "l"(a[0]), "l"(a[1]), "l"(a[2]), "l"(a[3]), "l"(b[0]), "l"(b[1]), "l"(b[2]),
+               "l"(b[3])
+               : "memory");
+}
+// A operand from TMEM (a[k] = TMEM addresses).
+__device__ __forceinline__ void mma_ts_x4(uint32_t d, const uint32_t (&a)[4], const uint64_t (&b)[4], uint32_t idesc,
+                                          uint32_t acc) {
+  asm volatile(ATTN_MMA_BATCH_HEAD
+               " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%3], %7, %1, p;\n"
+               " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%4], %8, %1, q;\n"
+               " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%5], %9, %1, q;\n"
+               " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%6], %10, %1, q;\n}\n" ::"r"(d),
+               "r"(idesc), "r"(acc), "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "l"(b[0]), "l"(b[1]), "l"(b[2]),
+               "l"(b[3])
+               : "memory");
+}
+__device__ __forceinline__ void mma_ts_x8(uint32_t d, const uint32_t (&a)[8], const uint64_t (&b)[8], uint32_t idesc,
+                                          uint32_t acc) {
+  asm volatile(ATTN_MMA_BATCH_HEAD
+               " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%3], %11, %1, p;\n"
+               " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%4], %12, %1, q;\n"
+               " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%5], %13, %1, q;\n"
+               " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%6], %14, %1, q;\n"
+               " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%7], %15, %1, q;\n"
+               " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%8], %16, %1, q;\n"
+               " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%9], %17, %1, q;\n"
+               " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%10], %18, %1, q;\n}\n" ::"r"(d),
+               "r"(idesc), "r"(acc), "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]),
+               "r"(a[7]), "l"(b[0]), "l"(b[1]), "l"(b[2]), "l"(b[3]), "l"(b[4]), "l"(b[5]), "l"(b[6]), "l"(b[7])
+               : "memory");
+}
+#undef ATTN_MMA_BATCH_HEAD
+
 __device__ __forceinline__ void mma_commit_warp(uint64_t* bar) {
   asm volatile(
       "{\n .reg .pred e;\n .reg .b32 r;\n elect.sync r|e, 0xffffffff;\n"

@@ -22,8 +22,8 @@ torch.cuda.synchronize()
 tr = np.zeros((32, 16), dtype=np.int64)
 ctypes.CDLL(lib_path).attn_debug_trace(tr.ctypes.data_as(ctypes.c_void_p))
 t0 = tr[3, 0]
-names = {12: "mma:V ready", 13: "mma:P0 seen", 15: "mma:K+1 ready", 14: "mma:P1 seen", 0: "mma:PV0 iss", 1: "mma:QK0+1 iss", 2: "mma:PV1 iss", 4: "sm0:wait S", 5: "sm0:S ready",
-         6: "sm0:exp start", 7: "sm0:P done", 8: "sm1:wait S", 9: "sm1:S ready", 10: "sm1:exp start", 11: "sm1:P done", 16: "w4 exp end", 17: "w5 exp end", 18: "w6 exp end", 19: "w7 exp end", 20: "w4 arrive", 21: "w5 arrive", 22: "w6 arrive", 23: "w7 arrive", 26: "sm0:S regs", 27: "sm0:max", 28: "sm0:o_done", 29: "sm1:S regs", 30: "sm1:max", 31: "sm1:o_done"}
+names = {24: "ld:K issue", 25: "ld:V issue", 12: "mma:V ready", 13: "mma:P0 seen", 15: "mma:K+1 ready", 14: "mma:P1 seen", 0: "mma:PV0 iss", 1: "mma:QK0+1 iss", 2: "mma:PV1 iss", 4: "sm0:wait S", 5: "sm0:S ready",
+         6: "sm0:exp start", 7: "sm0:P done", 8: "sm1:wait S", 9: "sm1:S ready", 10: "sm1:exp start", 11: "sm1:P done", 16: "q0 exp end", 17: "q1 exp end", 18: "q2 exp end", 19: "q3 exp end", 20: "q1:S ready", 21: "q1:S regs", 22: "q1:max", 23: "q1:exp start", 26: "sm0:S regs", 27: "sm0:max", 28: "sm0:o_done", 29: "sm1:S regs", 30: "sm1:max", 31: "sm1:o_done"}
 print("step " + " ".join(f"{names[e]:>13s}" for e in names))
 for j in range(min(16, S // 128 + 1)):
     print(f"{j:4d} " + " ".join(f"{((tr[e, j] - t0) & 0xffffffff) if tr[e, j] else 0:13d}" for e in names))
