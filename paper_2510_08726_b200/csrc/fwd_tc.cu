@@ -60,6 +60,9 @@ constexpr bool kTraceBuild = true;    // the timeline trace instruments the non-
 constexpr bool kTraceBuild = false;
 #endif
 
+#ifndef ATTN_ROLE_SWAP
+#define ATTN_ROLE_SWAP 1
+#endif
 #define WAIT_SM(bar, par) mbar_wait(bar, par)        // softmax waits: try_wait (HW sleep; test_wait polling: equal / -2.5 % at D = 64)
 #define WAIT_LM(bar, par) mbar_wait_spin(bar, par)   // loader / MMA thread waits: poll (try_wait: equal)
 
@@ -347,8 +350,15 @@ __global__ void __launch_bounds__(Roles<NT, bn_of<D>()>::kThreads, Roles<NT, bn_
   using C = Cfg<D, kExt, NT>;
   using Ro = Roles<NT, C::BNk>;
   constexpr int BN = C::BNk;   // KV tile width of this kernel (shadows the file constant)
-  constexpr int kSoftmaxWarps = Ro::kSoftmaxWarps, kWarpLoad = Ro::kWarpLoad, kWarpMma = Ro::kWarpMma;
-  constexpr int kWarpAlloc = Ro::kWarpAlloc;
+  constexpr int kSoftmaxWarps = Ro::kSoftmaxWarps;
+  // NT = 1 (several CTAs per SM): alternate the TMA-producer and MMA-issuer warps between the two
+  // extra warp ids by block parity, so co-resident CTAs spread their issuers over SM
+  // sub-partitions 0 and 1 (the issuer's sub-partition slows its softmax warps).
+  const bool swap_roles = NT == 1 && ATTN_ROLE_SWAP &&
+                          ((blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) & 1);
+  const int kWarpLoad = swap_roles ? Ro::kWarpMma : Ro::kWarpLoad;
+  const int kWarpMma = swap_roles ? Ro::kWarpLoad : Ro::kWarpMma;
+  const int kWarpAlloc = NT == 1 ? kWarpMma : Ro::kWarpAlloc;
   constexpr bool kPSmem = C::kPS;
   constexpr bool kF32x2 = D == 128;   // packed FFMA2 / FADD2 (measured: +1.5-2 % at D = 128, -4 % at D = 64)
   // (r1 alternated the two tiles' exp phases through a named-barrier token; r2 same-box A/B
