@@ -69,7 +69,9 @@ __global__ void __launch_bounds__(384, 1) k(const __grid_constant__ CUtensorMap 
       if (st_mode == 2) __nanosleep(100);
     }
   }
-  const int head = hbm_mode ? blockIdx.x : blockIdx.x % 16;   // hbm_mode: every CTA streams its own head
+  // hbm_mode 1: every CTA streams its own heads; 2: groups of 16 CTAs stream the same fresh heads in
+  // lockstep (the prefill kernel's q-blocks of one head); 3: as 2 plus an L2 prefetch 4 tiles ahead
+  const int head = hbm_mode == 1 ? blockIdx.x : hbm_mode >= 2 ? blockIdx.x / 16 : blockIdx.x % 16;
   const int tiles_per_pass = S / 128;
   long long t0 = clock64(), lat = 0;
   if (warp == 0 && lane == 0) {
@@ -80,7 +82,11 @@ __global__ void __launch_bounds__(384, 1) k(const __grid_constant__ CUtensorMap 
       mbar_arrive_expect_tx(&full[i % R], kTileBytes);
       uint8_t* dst = smem + (i % R) * kTileBytes;
       const int row = (i % tiles_per_pass) * 128;
-      const int hh = hbm_mode ? head + 148 * (i / tiles_per_pass) : head;   // never re-read
+      const int hh = hbm_mode == 1 ? head + 148 * (i / tiles_per_pass) : hbm_mode >= 2 ? head + 10 * (i / tiles_per_pass) : head;
+      if (hbm_mode == 3 && i + 4 < ntiles) {
+        const int i4 = i + 4, r4 = (i4 % tiles_per_pass) * 128, h4 = head + 10 * (i4 / tiles_per_pass);
+        for (int bx = 0; bx < 2; ++bx) tma_prefetch_4d(&tm, bx * 64, r4, h4, 0);
+      }
       for (int bx = 0; bx < 2; ++bx) tma_load_4d(&tm, &full[i % R], dst + bx * 16384, bx * 64, row, hh, 0, pol);
     }
   } else if (warp == 1 && lane == 0) {
@@ -110,7 +116,7 @@ void run(const CUtensorMap& tm, int S, int ntiles, int mma = 0, int hbm = 0, int
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
   double cyc = 0, lat = 0;
   for (int b = 0; b < 148; ++b) { cyc += h[2 * b] / 148.0; lat += h[2 * b + 1] / 148.0; }
-  printf("st %d %s mma %d ring %d x 32 KiB: %s  %.1f B/clk/SM (%.2f TB/s chip at 1.965 GHz)  mean issue->landed %.0f cyc\n", st, hbm ? "HBM" : "L2 ", mma, R,
+  printf("st %d mode %d mma %d ring %d x 32 KiB: %s  %.1f B/clk/SM (%.2f TB/s chip at 1.965 GHz)  mean issue->landed %.0f cyc\n", st, hbm, mma, R,
          cudaGetErrorString(e), (double)ntiles * kTileBytes / cyc, (double)ntiles * kTileBytes / cyc * 148 * 1.965e9 / 1e12,
          lat);
   cudaFree(d);
@@ -130,7 +136,11 @@ int main() {
                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) { printf("encode failed %d\n", (int)r); return 1; }
   const int ntiles = 512;
-  for (int st = 0; st < 3; ++st)
-    for (int mma = 0; mma < 3; ++mma) run<3>(tm, S, ntiles, mma, 0, st);
+  run<3>(tm, S, ntiles, 0, 0, 0);
+  run<3>(tm, S, 128, 0, 1, 0);
+  run<3>(tm, S, 128, 0, 2, 0);
+  run<3>(tm, S, 128, 0, 3, 0);
+  run<3>(tm, S, 128, 1, 2, 1);
+  run<3>(tm, S, 128, 1, 3, 1);
   return 0;
 }
