@@ -73,6 +73,14 @@ constexpr bool kTraceBuild = false;
 // 32-bit clock() samples (the host unwraps differences modulo 2^32).
 constexpr int kTrEv = 32, kTrSteps = 16;
 __device__ long long g_trace[kTrEv][kTrSteps];
+// per-CTA lifetime (trace builds, tools/cta_log.py): entry / exit globaltimer, SM id, clock64 cycles
+constexpr int kCtaLog = 8192;
+__device__ unsigned long long g_cta[kCtaLog][4];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ bool trace_cta() { return blockIdx.x == 5 && blockIdx.y == 3 && blockIdx.z == 2; }
 #define TRACE(ev, step)                                                          \
   do {                                                                           \
@@ -388,6 +396,16 @@ __global__ void __launch_bounds__(Roles<NT, bn_of<D>()>::kThreads, Roles<NT, bn_
 #endif
 
   const uint32_t warp = warp_id(), lane = lane_id();
+#ifdef ATTN_TRACE
+  const int cta_lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  if (threadIdx.x == 0 && cta_lin < kCtaLog) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    g_cta[cta_lin][0] = gtimer();
+    g_cta[cta_lin][2] = smid;
+    g_cta[cta_lin][3] = clock64();
+  }
+#endif
   // Block order.  Causal: heaviest q-blocks first -- across a GROUP of (head, batch) slices
   // whose K/V fit in kCausalL2Bytes of L2 (longest-processing-time order over the group),
   // not head by head: the hardware dispatches blocks in linear order, so a group's light
@@ -947,6 +965,10 @@ __global__ void __launch_bounds__(Roles<NT, bn_of<D>()>::kThreads, Roles<NT, bn_
   if (trace_cta())
     for (int i = threadIdx.x; i < kTrEv * kTrSteps; i += blockDim.x)
       g_trace[i / kTrSteps][i % kTrSteps] = s_trace[i];
+  if (threadIdx.x == 0 && cta_lin < kCtaLog) {
+    g_cta[cta_lin][1] = gtimer();
+    g_cta[cta_lin][3] = clock64() - g_cta[cta_lin][3];
+  }
 #endif
   if (warp == kWarpAlloc) {
     tc_fence_after();
@@ -1431,6 +1453,9 @@ cudaError_t launch_d(const FwdTcArgs& a, cudaStream_t stream) {
 }  // namespace
 
 #ifdef ATTN_TRACE
+extern "C" __attribute__((visibility("default"))) int attn_debug_cta_log(unsigned long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_cta, sizeof(g_cta));
+}
 extern "C" __attribute__((visibility("default"))) int attn_debug_trace(long long* host) {
   return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(g_trace));
 }
