@@ -182,7 +182,9 @@ __device__ __forceinline__ bool active(const Range& r, int j) { return j >= r.lo
 // +1 % (MHA), 4/16 -1 … -2 %,
 // 6/16 -8 % (the MUFU is not the binding unit there: the exp phase is paced by synchronisation,
 // DESIGN.md §4.1); ALiBi kernels keep MUFU only (2/16 -2 %, 4/16 -4 … -8 %).
-constexpr int kPolyGrid128 = 2, kPolyGrid64 = 2, kPolyPersist = 2;   // (ALiBi kernels: 0)
+// (r2, 4 CTAs/SM at D = 64: ALiBi 2/16 +0.4 … +0.9 % vs MUFU only; softcap 4/16 +1.4 %, the
+// others 4/16 -3 … -4 %, 1/16 -2 … -4 %.)
+constexpr int kPolyGrid128 = 2, kPolyGrid64 = 2, kPolyGrid64Cap = 4, kPolyPersist = 2;   // (D = 128 ALiBi: 0)
 template <int kPolyPairs>
 __device__ __forceinline__ constexpr bool poly_pair(int e) {
   return kPolyPairs > 0 && ((e * kPolyPairs) % 16) + kPolyPairs >= 16;
@@ -845,7 +847,7 @@ __global__ void __launch_bounds__(Roles<NT, bn_of<D>()>::kThreads, Roles<NT, bn_
             a1 = fmaf(x[c0 + 2 * e + 1], e_mul, e_add);
           }
           float p0, p1;
-          exp2_pair<kAlibi ? 0 : (D == 128 ? kPolyGrid128 : kPolyGrid64)>(a0, a1, p0, p1, e);
+          exp2_pair<D == 64 ? (kSoftcap ? kPolyGrid64Cap : kPolyGrid64) : (kAlibi ? 0 : kPolyGrid128)>(a0, a1, p0, p1, e);
           if constexpr (kF32x2) {
             add2_acc(sum0, sum1, p0, p1);
           } else {
