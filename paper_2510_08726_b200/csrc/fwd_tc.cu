@@ -60,9 +60,6 @@ constexpr bool kTraceBuild = true;    // the timeline trace instruments the non-
 constexpr bool kTraceBuild = false;
 #endif
 
-#ifndef ATTN_ROLE_SWAP
-#define ATTN_ROLE_SWAP 1
-#endif
 #define WAIT_SM(bar, par) mbar_wait(bar, par)        // softmax waits: try_wait (HW sleep; test_wait polling: equal / -2.5 % at D = 64)
 #define WAIT_LM(bar, par) mbar_wait_spin(bar, par)   // loader / MMA thread waits: poll (try_wait: equal)
 
@@ -371,7 +368,7 @@ __global__ void __launch_bounds__(Roles<NT, bn_of<D>()>::kThreads, Roles<NT, bn_
   // NT = 1 (several CTAs per SM): alternate the TMA-producer and MMA-issuer warps between the two
   // extra warp ids by block parity, so co-resident CTAs spread their issuers over SM
   // sub-partitions 0 and 1 (the issuer's sub-partition slows its softmax warps).
-  const bool swap_roles = NT == 1 && ATTN_ROLE_SWAP &&
+  const bool swap_roles = NT == 1 &&
                           ((blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) & 1);
   const int kWarpLoad = swap_roles ? Ro::kWarpMma : Ro::kWarpLoad;
   const int kWarpMma = swap_roles ? Ro::kWarpLoad : Ro::kWarpMma;
