@@ -23,10 +23,15 @@
 //     QK0(j+2), PV1(j), QK1(j+2) and S_t(j+1) is computed while the softmax of step j runs; K
 //     runs two tiles ahead of V in the ring.  (P aliasing S in TMEM with a TS MMA serialises
 //     softmax -> PV -> QK per tile: measured 3 % (r1, with the exp token) to 10 % (r2) slower.)
-//     Pure-causal problems run the persistent variant (fwd_tc_persist_kernel) of this layout.
+//     Pure-causal problems run the persistent variant (fwd_tc_persist_kernel) of this layout; it
+//     runs the MMA issuer on hardware warp 1 (the lowest id of its sub-partition) and the tile-0
+//     quarter-1 softmax warp on warp 9 (role_warp_persist).
 //   D = 64: CTA = ONE 128-row query tile, 64-key KV tiles, 192 threads (4 softmax warps, TMA
 //     producer, MMA issuer + TMEM allocator), TMEM S [0,64) (P aliasing it) + O [64,128): four
-//     CTAs per SM.
+//     CTAs per SM.  Producer and issuer alternate between the two extra warps by block parity,
+//     and the issuer trades ids with its sub-partition's softmax warp so it holds the lowest id.
+//   MMA issue: whole K loops as one batched asm block with one elect.sync (ptx.cuh mma_*_x4/x8)
+//     in the persistent and D = 64 kernels; the D = 128 grid kernel issues per MMA.
 //   Repair is lazy (reading R9): the reference max r' only moves when the
 //   running max exceeds it by more than kTau (log2 units); exact because h
 //   tag-updates to any reference (Eq. 6).
