@@ -65,6 +65,14 @@ constexpr bool kTraceBuild = true;    // the timeline trace instruments the non-
 constexpr bool kTraceBuild = false;
 #endif
 
+// D = 128 grid kernel: the MMA issue rotates over three warps (9, 10, 11 -> SM sub-partitions
+// 1, 2, 3) by KV step.  A warp blocked in tcgen05.mma issue slows the softmax warps of its own
+// sub-partition (the TMEM lane quarter there ran ~550 cycles/step behind, profiles/
+// r2_mma_issue_study.md); rotating spreads that over three quarters.  Same-box A/B (r2): MHA
+// +1.4 %, GQA window +0.6 %, ALiBi +1.0 %, ALiBi-causal +0.5 % (two issuers: +1.7 / +0.9 / +0.2 /
+// -0.8 %).  Every tcgen05.commit still covers only its own issuer's MMAs, which is all each
+// barrier needs (a step's K / V slots, S_t and O_t are produced within one step).
+constexpr int kGridIssuers = 3;
 #define WAIT_SM(bar, par) mbar_wait(bar, par)        // softmax waits: try_wait (HW sleep; test_wait polling: equal / -2.5 % at D = 64)
 #define WAIT_LM(bar, par) mbar_wait_spin(bar, par)   // loader / MMA thread waits: poll (try_wait: equal)
 
@@ -352,7 +360,7 @@ struct Roles {   // warp roles of fwd_tc_kernel
   static constexpr int kSoftmaxWarps = NT * kTileThreads / 32;
   static constexpr int kWarpLoad = kSoftmaxWarps, kWarpMma = kSoftmaxWarps + 1;
   static constexpr int kWarpAlloc = NT == 2 ? kSoftmaxWarps + 2 : kWarpMma;   // NT = 1: the MMA warp allocates
-  static constexpr int kThreads = (NT == 2 ? kSoftmaxWarps + 3 : kSoftmaxWarps + 2) * 32;
+  static constexpr int kThreads = (NT == 2 ? kSoftmaxWarps + (kGridIssuers > 2 ? 4 : 3) : kSoftmaxWarps + 2) * 32;
   // NT = 1: 2 CTAs per SM at 128-key tiles (256 TMEM columns each), 4 at 64-key tiles (128 each)
   static constexpr int kMinBlocks = NT == 2 ? 1 : (BNt == 64 ? 4 : 2);
   static constexpr int kTmemCols = NT == 2 ? 512 : (BNt == 64 ? 128 : 256);
@@ -598,7 +606,8 @@ __global__ void __launch_bounds__(Roles<NT, bn_of<D>()>::kThreads, Roles<NT, bn_
       }
       }
     }
-  } else if (warp == kWarpMma) {
+  } else if (warp == kWarpMma || (NT == 2 && kGridIssuers > 1 && warp > kWarpMma &&
+                                   warp < kWarpMma + kGridIssuers)) {
     // ------------------------------------------------------------ MMA issuer
     // The whole warp runs this role with warp-uniform values; one elected lane
     // issues each tcgen05 instruction (see mma_*_warp).
@@ -675,23 +684,34 @@ __global__ void __launch_bounds__(Roles<NT, bn_of<D>()>::kThreads, Roles<NT, bn_
           }
           mma_commit_warp(&o_done[t]);
         };
+        // KV step j is issued by issuer (j - ulo) % kNI, after the previous step's issuer has
+        // issued its last MMA (named barrier 12 + next issuer).
+        constexpr int kNI = NT == 2 ? kGridIssuers : 1;   // issuer warps (kWarpMma, +1, +2)
+        constexpr bool k2I = kNI > 1;
+        const int my = (int)warp - kWarpMma;
         int it = 0;
-        wait_tile(it);
-        if (active(rg[0], ulo)) qk_p(0, it, ulo);
-        if (active(rg[1], ulo)) qk_p(1, it, ulo);
-        mma_commit_warp(&kv_empty[it % C::kStages]);
+        if (my == 0) {
+          wait_tile(it);
+          if (active(rg[0], ulo)) qk_p(0, it, ulo);
+          if (active(rg[1], ulo)) qk_p(1, it, ulo);
+          mma_commit_warp(&kv_empty[it % C::kStages]);
+        }
         ++it;
         if (ulo + 1 < uhi) {
-          wait_tile(it);
-          if (active(rg[0], ulo + 1)) qk_p(0, it, ulo + 1);
-          if (active(rg[1], ulo + 1)) qk_p(1, it, ulo + 1);
-          mma_commit_warp(&kv_empty[it % C::kStages]);
+          if (my == 0) {
+            wait_tile(it);
+            if (active(rg[0], ulo + 1)) qk_p(0, it, ulo + 1);
+            if (active(rg[1], ulo + 1)) qk_p(1, it, ulo + 1);
+            mma_commit_warp(&kv_empty[it % C::kStages]);
+          }
           ++it;
         }
         for (int j = ulo; j < uhi; ++j) {
           const int itV = it++;
           const bool k2 = j + 2 < uhi;
           const int itK = k2 ? it++ : 0;
+          if (k2I && ((j - ulo) % kNI) != my) continue;
+          if (k2I && j > ulo) named_bar_sync(12 + my, 64);   // step j-1 is issued
           wait_tile(itV);
           if (lane == 0) TRACE(12, j);
           if (active(rg[0], j)) pv_p(0, itV, j > rg[0].lo);
@@ -708,6 +728,7 @@ __global__ void __launch_bounds__(Roles<NT, bn_of<D>()>::kThreads, Roles<NT, bn_
             if (active(rg[1], j + 2)) qk_p(1, itK, j + 2);
             mma_commit_warp(&kv_empty[itK % C::kStages]);
           }
+          if (k2I && j + 1 < uhi) named_bar_arrive(12 + ((j + 1 - ulo) % kNI), 64);
         }
       } else {
       wait_group(0);
