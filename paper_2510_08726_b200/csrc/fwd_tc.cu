@@ -9,12 +9,12 @@
 // O / l after the loop (Fig. 9 reverse_compute_at(norm)).
 //
 // B200 mapping:
-//   D = 128: CTA = 2 query tiles of BM = 128 rows of one (b, hq) -> 256 rows; 352 threads.
+//   D = 128: CTA = 2 query tiles of BM = 128 rows of one (b, hq) -> 256 rows; 384 threads.
 //     warps 0-3   : softmax/correction/epilogue for query tile 0 (thread = row)
 //     warps 4-7   : same for query tile 1
 //     warp 8      : TMA producer (Q once; K_j / V_j through a 3-slot ring of 128-key tiles)
-//     warp 9      : tcgen05.mma issuer (warp-wide, one elected lane issues)
-//     warp 10     : TMEM allocator (512 columns)
+//     warps 9-11  : tcgen05.mma issuers (warp-wide, one elected lane issues), rotating by KV
+//                   step (kGridIssuers); warp 10 also allocates TMEM (512 columns)
 //     The producer and MMA warps get the HIGHEST warp ids on purpose: the warp
 //     arbiter is highest-id-first, so they are never starved by the softmax warps.
 //     TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512) (fp32 columns).
